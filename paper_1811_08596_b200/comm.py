@@ -1,0 +1,141 @@
+"""Compressed gradient averaging across GPUs -- the exchange the reference
+only simulates by value (simulator.py:510-547: per-worker
+compress -> serialize -> deserialize -> decompress, then
+``v_hat = shard_weights @ recon``).
+
+One process per GPU.  Every rank compresses its own gradient into a
+fixed-capacity device message (count mode: capacity is known a priori, so no
+size exchange), one ``ncclAllGather`` moves all messages over NVLink /
+NVSwitch, and every rank decodes all W messages, accumulates
+``weight_w * X_w`` in the frequency domain in worker order and runs one
+inverse FFT per chunk.  The result is identical on every rank.
+
+Host-side logic (communicator bootstrap, layout agreement, weights) is
+separate from the transport so it can be exercised with the gloo backend on
+CPU (tests/test_comm_cpu.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _lib
+from .codec import CodecConfig, _desc, get_plan
+
+__all__ = ["message_layout", "shard_weights", "NcclComm", "GradientAverager", "allgather_average"]
+
+
+def message_layout(n: int, config: CodecConfig) -> tuple[int, int, np.ndarray]:
+    """(n_chunks, message_bytes, segment offsets) of the fixed-capacity
+    device message for a gradient of length n -- host-only, no GPU."""
+    spec = config.sparsification
+    d = _desc(n, config.chunk_size, spec.theta, spec.mode, config.half_precision_pass, config.quantizer, False)
+    nc = C.c_uint32()
+    nb = C.c_uint64()
+    _lib.check(_lib.lib.fgc_message_layout(C.byref(d), C.byref(nc), C.byref(nb), None))
+    offs = np.zeros(nc.value + 1, dtype=np.uint64)
+    _lib.check(_lib.lib.fgc_message_layout(C.byref(d), C.byref(nc), C.byref(nb), offs.ctypes.data))
+    return int(nc.value), int(nb.value), offs
+
+
+def shard_weights(batch_size: int, workers: int) -> np.ndarray:
+    """simulator.py:481-485: worker w averages shard_sizes[w] examples of an
+    np.array_split of the batch; weight = shard_size / batch_size."""
+    sizes = np.array([len(p) for p in np.array_split(np.arange(batch_size), workers)])
+    return sizes / batch_size
+
+
+class NcclComm:
+    """An NCCL communicator owned by libfgc_b200, bootstrapped through
+    torch.distributed (any backend) by broadcasting the unique id."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = np.zeros(128, dtype=np.uint8)
+        if self.rank == 0:
+            _lib.check(_lib.lib.fgc_nccl_unique_id(uid.ctypes.data))
+        obj = [uid.tobytes()]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        uid = np.frombuffer(obj[0], dtype=np.uint8).copy()
+        D.require_cuda()
+        h = C.c_void_p()
+        _lib.check(_lib.lib.fgc_nccl_comm_create(uid.ctypes.data, self.world, self.rank, C.byref(h)))
+        self.handle = h
+
+    def allgather(self, send: torch.Tensor, recv: torch.Tensor) -> None:
+        _lib.check(_lib.lib.fgc_allgather(self.handle, send.data_ptr(), recv.data_ptr(), send.numel(), D.stream()))
+
+    def allreduce_sum_(self, data: torch.Tensor) -> None:
+        _lib.check(_lib.lib.fgc_allreduce_sum_f32(self.handle, data.data_ptr(), data.numel(), D.stream()))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _lib.lib.fgc_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+
+class GradientAverager:
+    """Persistent buffers + plan for repeated compressed averaging of an
+    n-element gradient: the per-step call allocates nothing and launches
+    compress -> allgather -> decode-average on the current stream."""
+
+    def __init__(self, n: int, config: CodecConfig, weights, comm: NcclComm | None = None):
+        if config.sparsification.mode != "count":
+            raise NotImplementedError("energy-mode selection is not implemented on the GPU")
+        dev = D.require_cuda()
+        spec = config.sparsification
+        self.n = int(n)
+        self.config = config
+        self.comm = comm
+        self.world = 1 if comm is None else comm.world
+        w = np.asarray(weights, dtype=np.float64).reshape(-1)
+        if w.size != self.world:
+            raise ValueError(f"need one weight per rank ({self.world}), got {w.size}")
+        self.weights = np.ascontiguousarray(w)
+        self.plan = get_plan(self.n, config.chunk_size, spec.theta, spec.mode, config.half_precision_pass,
+                             config.quantizer)
+        self.message = self.plan.new_message()
+        self.gathered = (torch.empty(self.world * self.plan.message_bytes, dtype=torch.uint8, device=dev)
+                         if self.world > 1 else self.message)
+        self.out = torch.empty(self.n, dtype=torch.float32, device=dev)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def step(self, grad: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Average this rank's device gradient with every other rank's."""
+        if grad.numel() != self.n or not grad.is_cuda:
+            raise ValueError("gradient must be a CUDA tensor of the planned length")
+        code = _lib.DTYPE_F64 if grad.dtype == torch.float64 else _lib.DTYPE_F32
+        if grad.dtype not in (torch.float32, torch.float64):
+            raise ValueError("gradient must be float32 or float64")
+        dst = self.out if out is None else out
+        comm = None if self.comm is None else self.comm.handle
+        _lib.check(_lib.lib.fgc_allgather_average(self.plan.handle, comm, self.world, grad.data_ptr(), code,
+                                                  self.weights.ctypes.data, self.message.data_ptr(),
+                                                  self.gathered.data_ptr(), dst.data_ptr(), self.flags.data_ptr(),
+                                                  D.stream()))
+        return dst
+
+    def check(self) -> None:
+        """Raise the reference's ValueError if any step saw a bad gradient."""
+        f = D.read_flags(self.flags)
+        if f:
+            self.flags.zero_()
+            D.raise_on_flags(f)
+
+
+def allgather_average(local_grad, config: CodecConfig, weights, comm: NcclComm | None = None) -> np.ndarray:
+    """One compressed averaging step (simulator.py:520-547 across real GPUs):
+    returns ``sum_w weights[w] * decompress(compress(grad_w))`` as float64."""
+    t, code = D.as_signal(local_grad)
+    avg = GradientAverager(t.numel(), config, weights, comm)
+    out = avg.step(t if t.dtype in (torch.float32, torch.float64) else t.float())
+    avg.check()
+    return out.double().cpu().numpy()

@@ -1,0 +1,468 @@
+// Generic-length codec kernels: count-mode selection + quantize + pack from
+// a spectrum in global memory, and the decode + weighted accumulate of W
+// messages.  Used for tail chunks, any chunk length the fused kernels
+// (fused.cu) do not take, and the stage-injection entry point.
+//
+// Reference stages restated here:
+//   truncate, count mode    spectral.py:124-156 (stable argsort, k = ceil(theta*bins))
+//   _interleave + encode    codec.py:174-180, 197-202; quantizer.py:217-236
+//   pack + bitmap bytes     packer.py:41-58, 73-75; quantizer.py:266-273
+//   unpack + decode + avg   packer.py:61-70, quantizer.py:239-253, simulator.py:547
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "fgc_device.cuh"
+#include "fgc_internal.h"
+
+namespace fgc {
+
+namespace {
+
+inline uint32_t cdiv(uint64_t a, uint32_t b) { return (uint32_t)((a + b - 1) / b); }
+
+// ------------------------------------------------------------- select + pack
+
+constexpr int kSelThreads = 512;
+constexpr int kCandCap = 1024;
+constexpr uint32_t kHistBins = 2048;
+
+struct SelectShared {
+  uint32_t hist[kHistBins];
+  uint32_t scan[40];
+  unsigned long long key[kCandCap];
+  uint32_t idx[kCandCap];
+  uint32_t stage[2 * kSelThreads * 32 / 32 + 4];   // one tile of codes (<= 2T codes * 32 bits)
+  uint32_t cnt;
+  uint32_t found_bucket, found_below;
+};
+
+template <typename CT>
+struct Coeffs;
+template <>
+struct Coeffs<float2> {
+  const float2* p;
+  __device__ __forceinline__ void get(uint64_t i, float& re, float& im, double& dre, double& dim) const {
+    const float2 v = p[i];
+    re = v.x; im = v.y; dre = v.x; dim = v.y;
+  }
+};
+template <>
+struct Coeffs<double2> {
+  const double2* p;
+  __device__ __forceinline__ void get(uint64_t i, float& re, float& im, double& dre, double& dim) const {
+    const double2 v = p[i];
+    dre = v.x; dim = v.y; re = (float)v.x; im = (float)v.y;   // float32(coefficient)
+  }
+};
+
+// Bucket b such that below(b) <= r < below(b) + hist[b]; every thread returns it.
+__device__ void find_bucket(SelectShared& sh, uint32_t r, uint32_t& bucket, uint32_t& below) {
+  constexpr uint32_t per = kHistBins / kSelThreads;   // 4
+  uint32_t local = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < per; ++q) local += sh.hist[threadIdx.x * per + q];
+  uint32_t total;
+  uint32_t before = block_exclusive_scan<kSelThreads>(local, sh.scan, total);
+  if (r >= before && r < before + local) {
+    uint32_t acc = before;
+    for (uint32_t q = 0; q < per; ++q) {
+      const uint32_t h = sh.hist[threadIdx.x * per + q];
+      if (r < acc + h) {
+        sh.found_bucket = threadIdx.x * per + q;
+        sh.found_below = acc;
+        break;
+      }
+      acc += h;
+    }
+  }
+  __syncthreads();
+  bucket = sh.found_bucket;
+  below = sh.found_below;
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool key_less(unsigned long long ka, uint32_t ia, unsigned long long kb, uint32_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+// Bitonic sort of the first M (power of two) entries by (key, idx) or by idx.
+__device__ void bitonic(SelectShared& sh, uint32_t M, bool by_index) {
+  for (uint32_t k = 2; k <= M; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t t = threadIdx.x; t < M; t += blockDim.x) {
+        const uint32_t u = t ^ j;
+        if (u > t) {
+          const bool asc = (t & k) == 0;
+          bool greater;
+          if (by_index) greater = (sh.idx[t] & 0x7FFFFFFFu) > (sh.idx[u] & 0x7FFFFFFFu);
+          else greater = key_less(sh.key[u], sh.idx[u], sh.key[t], sh.idx[t]);
+          if (greater == asc) {
+            unsigned long long tk = sh.key[t]; sh.key[t] = sh.key[u]; sh.key[u] = tk;
+            uint32_t ti = sh.idx[t]; sh.idx[t] = sh.idx[u]; sh.idx[u] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+enum SelMode : int { kKeepAll = 0, kDropAll = 1, kList = 2, kExact = 3 };
+
+template <typename CT>
+__global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* chunks, uint32_t first, Coeffs<CT> coeffs,
+                                                             int exact_only, QuantParams q, uint8_t* message,
+                                                             uint8_t* kept_mask, uint32_t* flags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SelectShared& sh = *reinterpret_cast<SelectShared*>(smem_raw);
+  const ChunkInfo ci = chunks[first + blockIdx.x];
+  const uint32_t B = ci.bins;
+  const uint32_t kdrop = ci.drop;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Coeffs<CT> cf = coeffs;
+  cf.p += ci.bin_off;
+
+  int mode = kList;
+  if (kdrop == 0) mode = kKeepAll;
+  else if (kdrop >= B) mode = kDropAll;
+
+  float band_lo = 0.f, band_hi = INFINITY;   // proxy band of undecided bins
+  bool all_band = false;
+  uint32_t need = 0, m = 0;
+  unsigned long long Te = 0;                  // exact mode threshold key
+  uint32_t tie_cut = 0;
+
+  if (mode == kList) {
+    if (exact_only) {
+      all_band = true;
+    } else {
+      const uint32_t r = kdrop - 1;             // rank of the largest dropped bin
+      // pass 1: proxy bits [30:20]
+      for (uint32_t b = tid; b < kHistBins; b += kSelThreads) sh.hist[b] = 0;
+      __syncthreads();
+      for (uint32_t i = tid; i < B; i += kSelThreads) {
+        float re, im; double dr, di;
+        cf.get(i, re, im, dr, di);
+        atomicAdd(&sh.hist[__float_as_uint(proxy_key(re, im)) >> 20], 1u);
+      }
+      __syncthreads();
+      uint32_t b1, below1;
+      find_bucket(sh, r, b1, below1);
+      // pass 2: proxy bits [19:9] inside bucket b1
+      for (uint32_t b = tid; b < kHistBins; b += kSelThreads) sh.hist[b] = 0;
+      __syncthreads();
+      for (uint32_t i = tid; i < B; i += kSelThreads) {
+        float re, im; double dr, di;
+        cf.get(i, re, im, dr, di);
+        const uint32_t pb = __float_as_uint(proxy_key(re, im));
+        if ((pb >> 20) == b1) atomicAdd(&sh.hist[(pb >> 9) & 0x7FFu], 1u);
+      }
+      __syncthreads();
+      uint32_t b2, below2;
+      find_bucket(sh, r - below1, b2, below2);
+      const uint32_t lo_pat = (b1 << 20) | (b2 << 9);
+      const float lo_f = __uint_as_float(lo_pat);
+      const float hi_f = __uint_as_float(lo_pat + 512u);
+      if (lo_f < 0x1p-100f || hi_f > 0x1p100f) {
+        all_band = true;                          // proxy unreliable: decide exactly
+      } else {
+        band_lo = lo_f * (1.0f - 0x1p-16f);
+        band_hi = hi_f * (1.0f + 0x1p-16f);
+      }
+    }
+    // collect the undecided band; count the certainly-dropped bins below it
+    if (tid == 0) sh.cnt = 0;
+    __syncthreads();
+    uint32_t below_local = 0;
+    for (uint32_t i = tid; i < B; i += kSelThreads) {
+      float re, im; double dr, di;
+      cf.get(i, re, im, dr, di);
+      const float p = proxy_key(re, im);
+      if (!all_band && p < band_lo) {
+        ++below_local;
+      } else if (all_band || p < band_hi) {
+        const uint32_t s = atomicAdd(&sh.cnt, 1u);
+        if (s < kCandCap) sh.idx[s] = i;
+      }
+    }
+    const uint32_t below = block_sum<kSelThreads>(below_local, sh.scan);
+    m = sh.cnt;
+    need = kdrop - below;
+    if (m <= (uint32_t)kCandCap) {
+      uint32_t M = 1;
+      while (M < m) M <<= 1;
+      for (uint32_t s = tid; s < M; s += kSelThreads) {
+        if (s < m) {
+          float re, im; double dr, di;
+          cf.get(sh.idx[s], re, im, dr, di);
+          sh.key[s] = (unsigned long long)__double_as_longlong(cabs_key(dr, di));
+        } else {
+          sh.key[s] = ~0ull;
+          sh.idx[s] = 0x7FFFFFFFu;
+        }
+      }
+      __syncthreads();
+      bitonic(sh, M, false);
+      for (uint32_t s = tid; s < m; s += kSelThreads)
+        if (s < need) sh.idx[s] |= 0x80000000u;  // mark dropped
+      __syncthreads();
+      bitonic(sh, M, true);
+    } else {
+      mode = kExact;
+      // radix select over the 63-bit exact key among band bins
+      unsigned long long prefix = 0, pmask = 0;
+      uint32_t rr = need ? need - 1 : 0, c_less = 0;
+      const int shifts[6] = {52, 41, 30, 19, 8, 0};
+      const int widths[6] = {11, 11, 11, 11, 11, 8};
+      if (need > 0) {
+        for (int pass = 0; pass < 6; ++pass) {
+          for (uint32_t b = tid; b < kHistBins; b += kSelThreads) sh.hist[b] = 0;
+          __syncthreads();
+          const unsigned long long dm = (1ull << widths[pass]) - 1ull;
+          for (uint32_t i = tid; i < B; i += kSelThreads) {
+            float re, im; double dr, di;
+            cf.get(i, re, im, dr, di);
+            const float p = proxy_key(re, im);
+            if (!(all_band || (p >= band_lo && p < band_hi))) continue;
+            const unsigned long long key = (unsigned long long)__double_as_longlong(cabs_key(dr, di));
+            if ((key & pmask) == prefix) atomicAdd(&sh.hist[(key >> shifts[pass]) & dm], 1u);
+          }
+          __syncthreads();
+          uint32_t bk, bl;
+          find_bucket(sh, rr, bk, bl);
+          prefix |= (unsigned long long)bk << shifts[pass];
+          pmask |= dm << shifts[pass];
+          rr -= bl;
+          c_less += bl;
+        }
+        Te = prefix;
+        tie_cut = need - c_less;
+      }
+    }
+  }
+
+  // ---- final pass: decide, quantize, bitmap + code stream (tile-sequential)
+  uint32_t* seg = reinterpret_cast<uint32_t*>(message + ci.seg_off);
+  uint32_t* bitmap = seg + kSegHeader / 4;
+  uint32_t* codes = reinterpret_cast<uint32_t*>(message + ci.seg_off + ci.code_off);
+  const uint32_t bm_words = (ci.slots + 31) / 32;
+  const int N = q.n_bits;
+  uint32_t rank_base = 0;     // codes emitted so far
+  uint32_t origin = 0;        // global code word index of stage[0]
+  uint32_t tie_seen = 0;
+  bool overflow = false;
+  const uint32_t stage_words = 2 * kSelThreads * 32 / 32 + 4;
+  for (uint32_t s = tid; s < stage_words; s += kSelThreads) sh.stage[s] = 0;
+  __syncthreads();
+
+  for (uint32_t t0 = 0; t0 < B; t0 += kSelThreads) {
+    const uint32_t i = t0 + tid;
+    const bool valid = i < B;
+    float re = 0.f, im = 0.f; double dr = 0.0, di = 0.0;
+    if (valid) cf.get(i, re, im, dr, di);
+    bool dropped = false;
+    bool is_tie = false;
+    unsigned long long key = 0;
+    if (mode == kDropAll) {
+      dropped = true;
+    } else if (mode == kList || mode == kExact) {
+      const float p = proxy_key(re, im);
+      const bool inband = all_band || (p >= band_lo && p < band_hi);
+      if (!all_band && p < band_lo) dropped = true;
+      else if (inband && valid) {
+        if (mode == kList) {
+          uint32_t lo = 0, hi = m;                 // binary search by index
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((sh.idx[mid] & 0x7FFFFFFFu) < i) lo = mid + 1; else hi = mid;
+          }
+          dropped = (lo < m) && ((sh.idx[lo] & 0x7FFFFFFFu) == i) && (sh.idx[lo] & 0x80000000u);
+        } else if (need > 0) {
+          key = (unsigned long long)__double_as_longlong(cabs_key(dr, di));
+          dropped = key < Te;
+          is_tie = key == Te;
+        }
+      }
+    }
+    if (mode == kExact) {
+      uint32_t ties_total;
+      const uint32_t tie_rank = tie_seen + block_exclusive_scan<kSelThreads>(is_tie ? 1u : 0u, sh.scan, ties_total);
+      if (is_tie) dropped = tie_rank < tie_cut;
+      tie_seen += ties_total;
+    }
+    if (!valid) dropped = true;
+    const uint32_t cre = dropped ? 0u : encode_code(q, re);
+    const uint32_t cim = dropped ? 0u : encode_code(q, im);
+    if (kept_mask && valid) kept_mask[ci.bin_off + i] = dropped ? 0 : 1;
+
+    const uint32_t bre = __ballot_sync(0xffffffffu, cre != 0u);
+    const uint32_t bim = __ballot_sync(0xffffffffu, cim != 0u);
+    // bitmap words for the warp's 64 slots
+    if (lane < 2) {
+      const uint32_t rh = lane ? (bre >> 16) : (bre & 0xFFFFu);
+      const uint32_t ih = lane ? (bim >> 16) : (bim & 0xFFFFu);
+      const uint32_t w = spread16(rh) | (spread16(ih) << 1);
+      const uint32_t widx = (t0 + warp * 32) / 16 + lane;
+      if (widx < bm_words) bitmap[widx] = ballot_to_wire(w);
+    }
+    // ranks
+    const uint32_t lt = lanemask_lt();
+    const uint32_t pre = __popc(bre & lt) + __popc(bim & lt);
+    const uint32_t wtot = __popc(bre) + __popc(bim);
+    if (lane == 0) sh.scan[warp] = wtot;
+    __syncthreads();
+    uint32_t wbase = 0, ttot = 0;
+    for (int w = 0; w < kSelThreads / 32; ++w) {
+      const uint32_t v = sh.scan[w];
+      if (w < warp) wbase += v;
+      ttot += v;
+    }
+    const uint32_t r0 = rank_base + wbase + pre;
+    // stage the codes (LSB-first N-bit fields, bit 0 of stage[0] = word `origin`)
+    const uint64_t obit = (uint64_t)origin * 32u;
+    if (cre) {
+      const uint64_t lb = (uint64_t)r0 * N - obit;
+      const uint32_t o = (uint32_t)(lb & 31u);
+      atomicOr(&sh.stage[lb >> 5], cre << o);
+      if (o + N > 32u) atomicOr(&sh.stage[(lb >> 5) + 1], cre >> (32u - o));
+    }
+    if (cim) {
+      const uint64_t lb = (uint64_t)(r0 + (cre ? 1u : 0u)) * N - obit;
+      const uint32_t o = (uint32_t)(lb & 31u);
+      atomicOr(&sh.stage[lb >> 5], cim << o);
+      if (o + N > 32u) atomicOr(&sh.stage[(lb >> 5) + 1], cim >> (32u - o));
+    }
+    __syncthreads();
+    const uint64_t end_bit = (uint64_t)(rank_base + ttot) * N;
+    const uint32_t full_end = (uint32_t)(end_bit >> 5);      // words [origin, full_end) complete
+    for (uint32_t w = origin + tid; w < full_end; w += kSelThreads) {
+      if (w < ci.code_cap) codes[w] = sh.stage[w - origin];
+      else overflow = true;
+    }
+    const uint32_t carry = (full_end >= origin) ? sh.stage[full_end - origin] : 0u;
+    __syncthreads();
+    for (uint32_t s = tid; s < stage_words; s += kSelThreads) sh.stage[s] = 0;
+    __syncthreads();
+    if (tid == 0) sh.stage[0] = carry;
+    origin = full_end;
+    rank_base += ttot;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if ((uint64_t)rank_base * N & 31u) {
+      if (origin < ci.code_cap) codes[origin] = sh.stage[0];
+      else overflow = true;
+    }
+    seg[0] = rank_base;
+    seg[1] = 0; seg[2] = 0; seg[3] = 0;
+  }
+  // zero the bitmap tail words beyond the last tile (none: tiles cover bins)
+  if (overflow) atomicOr(flags, FGC_FLAG_CAPACITY);
+}
+
+// ------------------------------------------------------------- decode + accumulate
+
+constexpr int kDecThreads = 512;
+
+__global__ void __launch_bounds__(kDecThreads) k_decode_accumulate(const ChunkInfo* chunks, uint32_t first,
+                                                                   const uint8_t* messages, int W, int w0, int G,
+                                                                   uint64_t stride, Weights wts, QuantParams q,
+                                                                   float2* spectrum) {
+  extern __shared__ __align__(16) uint32_t pref[];    // G x bm_words exclusive popcount prefixes
+  __shared__ uint32_t scan[40];
+  const ChunkInfo ci = chunks[first + blockIdx.x];
+  const uint32_t bm_words = (ci.slots + 31) / 32;
+  const uint32_t tid = threadIdx.x;
+  const int gn = min(G, W - w0);
+  // prefix tables: each thread owns a contiguous run of words
+  const uint32_t per = (bm_words + kDecThreads - 1) / kDecThreads;
+  for (int g = 0; g < gn; ++g) {
+    const uint32_t* bm = reinterpret_cast<const uint32_t*>(messages + (uint64_t)(w0 + g) * stride + ci.seg_off + kSegHeader);
+    uint32_t local = 0;
+    const uint32_t a = tid * per, b = min(bm_words, a + per);
+    for (uint32_t w = a; w < b; ++w) local += __popc(bm[w]);
+    uint32_t tot;
+    uint32_t base = block_exclusive_scan<kDecThreads>(local, scan, tot);
+    for (uint32_t w = a; w < b; ++w) {
+      pref[g * bm_words + w] = base;
+      base += __popc(bm[w]);
+    }
+  }
+  __syncthreads();
+  const int N = q.n_bits;
+  for (uint32_t i = tid; i < ci.bins; i += kDecThreads) {
+    float2 acc = make_float2(0.f, 0.f);
+    if (w0 > 0) acc = spectrum[ci.bin_off + i];
+    const uint32_t slot = 2 * i;
+    const uint32_t word = slot >> 5, sh = slot & 31u;
+    for (int g = 0; g < gn; ++g) {
+      const uint8_t* seg = messages + (uint64_t)(w0 + g) * stride + ci.seg_off;
+      const uint32_t* bm = reinterpret_cast<const uint32_t*>(seg + kSegHeader);
+      const uint32_t* cw = reinterpret_cast<const uint32_t*>(seg + ci.code_off);
+      const uint32_t sw = ballot_to_wire(bm[word]);          // slot order
+      const uint32_t bits = (sw >> sh) & 3u;
+      if (!bits) continue;
+      uint32_t r = pref[g * bm_words + word] + __popc(sw & ((1u << sh) - 1u));
+      float re = 0.f, im = 0.f;
+      if (bits & 1u) { re = decode_code(q, read_bits(cw, (uint64_t)r * N, N)); ++r; }
+      if (bits & 2u) im = decode_code(q, read_bits(cw, (uint64_t)r * N, N));
+      const float wt = wts.w[w0 + g];
+      acc.x = __fmaf_rn(wt, re, acc.x);
+      acc.y = __fmaf_rn(wt, im, acc.y);
+    }
+    spectrum[ci.bin_off + i] = acc;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- launchers
+
+fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_t count, const void* spectrum,
+                              int coeff_f64, const QuantParams& q, uint8_t* message, uint8_t* kept_mask,
+                              uint32_t* flags, cudaStream_t s) {
+  if (!count) return FGC_OK;
+  static bool attr = false;
+  const size_t smem = sizeof(SelectShared);
+  if (!attr) {
+    FGC_CUDA(cudaFuncSetAttribute(k_select_pack<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FGC_CUDA(cudaFuncSetAttribute(k_select_pack<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  if (coeff_f64) {
+    Coeffs<double2> c{static_cast<const double2*>(spectrum)};
+    k_select_pack<double2><<<count, kSelThreads, smem, s>>>(d_chunks, first, c, 1, q, message, kept_mask, flags);
+  } else {
+    Coeffs<float2> c{static_cast<const float2*>(spectrum)};
+    k_select_pack<float2><<<count, kSelThreads, smem, s>>>(d_chunks, first, c, 0, q, message, kept_mask, flags);
+  }
+  FGC_LAUNCHED(1);
+  return FGC_OK;
+}
+
+fgc_status launch_decode_accumulate(const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                                    const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
+                                    const QuantParams& q, float2* spectrum, uint32_t max_slots, cudaStream_t s) {
+  if (!count) return FGC_OK;
+  const uint32_t bm_words = (max_slots + 31) / 32;
+  const size_t budget = 200 * 1024;
+  const size_t gmax = budget / (bm_words * 4ull);
+  int G = (int)((size_t)W < gmax ? (size_t)W : gmax);
+  if (G < 1) {
+    set_error("chunk too large for the decode prefix tables");
+    return FGC_ERR_UNSUPPORTED;
+  }
+  static bool attr = false;
+  if (!attr) {
+    FGC_CUDA(cudaFuncSetAttribute(k_decode_accumulate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
+    attr = true;
+  }
+  for (int w0 = 0; w0 < W; w0 += G) {
+    const size_t smem = (size_t)G * bm_words * 4;
+    k_decode_accumulate<<<count, kDecThreads, smem, s>>>(d_chunks, first, messages, W, w0, G, stride, wts, q, spectrum);
+    FGC_LAUNCHED(1);
+  }
+  return FGC_OK;
+}
+
+}  // namespace fgc

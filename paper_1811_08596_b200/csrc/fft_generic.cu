@@ -1,0 +1,317 @@
+// Generic batched complex DFT engine, float32 or float64.  It takes every
+// transform the fused kernels do not: tail chunks, non-power-of-two chunk
+// sizes, and the whole-signal primitives (dft_forward / dft_inverse /
+// calibrate, which the reference computes in float64 with numpy's pocketfft:
+// spectral.py:95,106, codec.py:463).
+//
+//   Direct     Lc <= 64            O(Lc^2) per signal, exact-reduced twiddles
+//   Pow2       Lc = 2^k            Stockham radix-2 in shared memory (<= 4096
+//                                  points), larger sizes by a four-step split
+//                                  through global memory (recursive on rows)
+//   Bluestein  anything else        chirp-z convolution on a Pow2 engine of
+//                                  size P >= 2 Lc - 1
+//
+// Twiddles/chirps are evaluated in float64 with the angle reduced exactly in
+// integers, then stored in the engine precision.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "fgc_device.cuh"
+#include "fgc_internal.h"
+
+namespace fgc {
+
+namespace {
+
+constexpr int kFftThreads = 256;
+
+template <class R> struct V2;
+template <> struct V2<float> { using T = float2; };
+template <> struct V2<double> { using T = double2; };
+
+__device__ __forceinline__ float2 mk(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ double2 mk(double x, double y) { return make_double2(x, y); }
+
+__device__ __forceinline__ float2 zmul(float2 a, float2 b) { return cmul(a, b); }
+__device__ __forceinline__ double2 zmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+template <class T2> __device__ __forceinline__ T2 zconj(T2 a) { return mk(a.x, -a.y); }
+template <class T2> __device__ __forceinline__ T2 zadd(T2 a, T2 b) { return mk(a.x + b.x, a.y + b.y); }
+template <class T2> __device__ __forceinline__ T2 zsub(T2 a, T2 b) { return mk(a.x - b.x, a.y - b.y); }
+
+template <class R>
+__global__ void k_init_twiddles(typename V2<R>::T* tw, uint32_t P) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P) return;
+  double s, c;
+  sincospi(-2.0 * (double)j / (double)P, &s, &c);
+  tw[j] = mk((R)c, (R)s);
+}
+
+template <class R>
+__global__ void k_init_chirp(typename V2<R>::T* chirp, uint32_t Lc) {
+  uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Lc) return;
+  const uint64_t m = ((uint64_t)n * n) % (2ull * Lc);       // exact angle reduction
+  double s, c;
+  sincospi(-(double)m / (double)Lc, &s, &c);
+  chirp[n] = mk((R)c, (R)s);
+}
+
+template <class R>
+__global__ void k_init_bluestein_b(typename V2<R>::T* b, const typename V2<R>::T* chirp, uint32_t P, uint32_t Lc) {
+  uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= P) return;
+  typename V2<R>::T v = mk((R)0, (R)0);
+  if (e < Lc) v = zconj(chirp[e]);
+  else if (P - e < Lc) v = zconj(chirp[P - e]);
+  b[e] = v;
+}
+
+// Stockham radix-2 over `nt` transforms of size S held in shared memory.
+template <class T2>
+__device__ T2* smem_stockham(T2* x, T2* y, uint32_t S, uint32_t nt, const T2* tw, uint32_t twP, int dir) {
+  const uint32_t half = S >> 1;
+  const uint32_t lhalf = __ffs(half) - 1;
+  for (uint32_t p = 1; p < S; p <<= 1) {
+    const uint32_t twstride = twP / (2 * p);
+    for (uint32_t b = threadIdx.x; b < nt * half; b += blockDim.x) {
+      const uint32_t t = b >> lhalf, i = b & (half - 1);
+      const uint32_t k = i & (p - 1);
+      const T2 u0 = x[t * S + i];
+      T2 w = tw[(uint64_t)k * twstride];
+      if (dir > 0) w.y = -w.y;
+      const T2 u1 = zmul(x[t * S + i + half], w);
+      const uint32_t o = t * S + ((i - k) << 1) + k;
+      y[o] = zadd(u0, u1);
+      y[o + p] = zsub(u0, u1);
+    }
+    __syncthreads();
+    T2* tmp = x; x = y; y = tmp;
+  }
+  return x;
+}
+
+// Batched transforms of size S <= kSmemFftMax stored contiguously.
+template <class T2>
+__global__ void __launch_bounds__(kFftThreads) k_smem_fft(T2* data, uint32_t S, uint32_t per_cta, uint64_t total,
+                                                          const T2* tw, uint32_t twP, int dir) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T2* sm = reinterpret_cast<T2*>(smraw);
+  const uint64_t first = (uint64_t)blockIdx.x * per_cta;
+  if (first >= total) return;
+  const uint32_t nt = (uint32_t)min((uint64_t)per_cta, total - first);
+  T2* x = sm;
+  T2* y = sm + (size_t)per_cta * S;
+  T2* g = data + first * S;
+  for (uint32_t e = threadIdx.x; e < nt * S; e += blockDim.x) x[e] = g[e];
+  __syncthreads();
+  T2* r = smem_stockham(x, y, S, nt, tw, twP, dir);
+  for (uint32_t e = threadIdx.x; e < nt * S; e += blockDim.x) g[e] = r[e];
+}
+
+// Four-step column pass over an R x C matrix per item (item stride R*C):
+// G columns per CTA, a length-R FFT down each, with the inter-step twiddle
+// W_{RC}^{c k1} after (forward) or before (inverse) the column transform.
+template <class T2>
+__global__ void __launch_bounds__(kFftThreads) k_col_fft(T2* data, uint32_t Rr, uint32_t C, uint32_t G, const T2* tw,
+                                                         uint32_t twP, int dir) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T2* sm = reinterpret_cast<T2*>(smraw);
+  const uint32_t groups = C / G;
+  const uint64_t P = (uint64_t)Rr * C;
+  const uint64_t item = blockIdx.x / groups;
+  const uint32_t c0 = (blockIdx.x % groups) * G;
+  const uint32_t tws = (uint32_t)(twP / P);   // table is for twP >= P
+  T2* g = data + item * P;
+  T2* x = sm;
+  T2* y = sm + (size_t)G * Rr;
+  for (uint32_t e = threadIdx.x; e < G * Rr; e += blockDim.x) {
+    const uint32_t r = e / G, cg = e % G;            // coalesced along columns
+    T2 v = g[(uint64_t)r * C + c0 + cg];
+    if (dir > 0) {
+      T2 w = tw[(((uint64_t)(c0 + cg) * r) % P) * tws];
+      w.y = -w.y;
+      v = zmul(v, w);
+    }
+    x[cg * Rr + r] = v;
+  }
+  __syncthreads();
+  T2* res = smem_stockham(x, y, Rr, G, tw, twP, dir);
+  for (uint32_t e = threadIdx.x; e < G * Rr; e += blockDim.x) {
+    const uint32_t r = e / G, cg = e % G;
+    T2 v = res[cg * Rr + r];
+    if (dir < 0) v = zmul(v, tw[(((uint64_t)(c0 + cg) * r) % P) * tws]);
+    g[(uint64_t)r * C + c0 + cg] = v;
+  }
+}
+
+// Direct DFT for Lc <= 64: out[k] = sum_n in[n] exp(dir * 2 pi i n k / Lc).
+template <class R>
+__global__ void k_direct_dft(const typename V2<R>::T* in, typename V2<R>::T* out, uint32_t Lc, int dir) {
+  using T2 = typename V2<R>::T;
+  __shared__ T2 z[64];
+  __shared__ T2 w[64];
+  const T2* src = in + (uint64_t)blockIdx.x * Lc;
+  T2* dst = out + (uint64_t)blockIdx.x * Lc;
+  for (uint32_t n = threadIdx.x; n < Lc; n += blockDim.x) {
+    z[n] = src[n];
+    double s, c;
+    sincospi((double)dir * 2.0 * (double)n / (double)Lc, &s, &c);
+    w[n] = mk((R)c, (R)s);
+  }
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < Lc; k += blockDim.x) {
+    T2 acc = mk((R)0, (R)0);
+    uint32_t idx = 0;
+    for (uint32_t n = 0; n < Lc; ++n) {
+      acc = zadd(acc, zmul(z[n], w[idx]));
+      idx += k;
+      if (idx >= Lc) idx -= Lc;
+    }
+    dst[k] = acc;
+  }
+}
+
+template <class T2>
+__global__ void k_pointwise_mul(T2* data, const T2* f, uint32_t P, uint64_t total) {
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  data[e] = zmul(data[e], f[e % P]);
+}
+
+inline uint32_t ceil_div(uint64_t a, uint32_t b) { return (uint32_t)((a + b - 1) / b); }
+
+template <class R>
+fgc_status pow2_rec(typename V2<R>::T* data, uint64_t batch, uint32_t P, const typename V2<R>::T* tw, uint32_t twP,
+                    int dir, cudaStream_t s) {
+  using T2 = typename V2<R>::T;
+  if (P <= 1 || batch == 0) return FGC_OK;
+  const uint32_t cap = smem_points(sizeof(R));   // points per CTA, held twice in 64 KB
+  if (P <= cap) {
+    const uint32_t per = max(1u, cap / P);
+    const size_t smem = 2ull * per * P * sizeof(T2);
+    k_smem_fft<T2><<<ceil_div(batch, per), kFftThreads, smem, s>>>(data, P, per, batch, tw, twP, dir);
+    FGC_LAUNCHED(1);
+    return FGC_OK;
+  }
+  uint32_t Rr, C;
+  fft_split(P, cap, Rr, C);
+  const uint32_t G = max(1u, min(C, cap / Rr));
+  const size_t col_smem = 2ull * G * Rr * sizeof(T2);
+  const uint64_t cols = batch * (C / G);
+  if (cols > 0x7FFFFFFFull) { set_error("transform batch too large"); return FGC_ERR_UNSUPPORTED; }
+  if (dir < 0) {
+    k_col_fft<T2><<<(uint32_t)cols, kFftThreads, col_smem, s>>>(data, Rr, C, G, tw, twP, dir);
+    FGC_LAUNCHED(1);
+    FGC_TRY(pow2_rec<R>(data, batch * Rr, C, tw, twP, dir, s));
+  } else {
+    FGC_TRY(pow2_rec<R>(data, batch * Rr, C, tw, twP, dir, s));
+    k_col_fft<T2><<<(uint32_t)cols, kFftThreads, col_smem, s>>>(data, Rr, C, G, tw, twP, dir);
+    FGC_LAUNCHED(1);
+  }
+  return FGC_OK;
+}
+
+uint32_t next_pow2(uint64_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+template <class R>
+fgc_status set_attrs() {
+  using T2 = typename V2<R>::T;
+  static bool done = false;
+  if (done) return FGC_OK;
+  const int bytes = (int)(2 * smem_points(sizeof(R)) * sizeof(T2));
+  FGC_CUDA(cudaFuncSetAttribute(k_smem_fft<T2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  FGC_CUDA(cudaFuncSetAttribute(k_col_fft<T2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done = true;
+  return FGC_OK;
+}
+
+}  // namespace
+
+template <class R>
+fgc_status DftPlanT<R>::init(uint32_t Lc_, uint32_t batch_, cudaStream_t s) {
+  FGC_TRY(set_attrs<R>());
+  Lc = Lc_;
+  batch = batch_;
+  if (Lc <= 64) {
+    kind = DftKind::Direct;
+    P = Lc;
+  } else if ((Lc & (Lc - 1)) == 0) {
+    kind = DftKind::Pow2;
+    P = Lc;
+  } else {
+    kind = DftKind::Bluestein;
+    if (2ull * Lc - 1 > (1ull << 31)) { set_error("DFT length too large"); return FGC_ERR_UNSUPPORTED; }
+    P = next_pow2(2ull * Lc - 1);
+  }
+  if (kind != DftKind::Direct) {
+    FGC_CUDA(cudaMalloc(&tw, sizeof(T2) * P));
+    k_init_twiddles<R><<<ceil_div(P, 256), 256, 0, s>>>(tw, P);
+    FGC_LAUNCHED(1);
+  }
+  if (batch) {
+    FGC_CUDA(cudaMalloc(&work, sizeof(T2) * (uint64_t)P * batch));
+    if (kind == DftKind::Direct) FGC_CUDA(cudaMalloc(&work2, sizeof(T2) * (uint64_t)P * batch));
+  }
+  if (kind == DftKind::Bluestein) {
+    FGC_CUDA(cudaMalloc(&chirp, sizeof(T2) * Lc));
+    FGC_CUDA(cudaMalloc(&bf, sizeof(T2) * P));
+    k_init_chirp<R><<<ceil_div(Lc, 256), 256, 0, s>>>(chirp, Lc);
+    FGC_LAUNCHED(1);
+    k_init_bluestein_b<R><<<ceil_div(P, 256), 256, 0, s>>>(bf, chirp, P, Lc);
+    FGC_LAUNCHED(1);
+    FGC_TRY(pow2_rec<R>(bf, 1, P, tw, P, -1, s));
+  }
+  return FGC_OK;
+}
+
+template <class R>
+void DftPlanT<R>::free_all() {
+  cudaFree(tw);
+  cudaFree(chirp);
+  cudaFree(bf);
+  cudaFree(work);
+  cudaFree(work2);
+  cudaFree(rtw);
+  tw = chirp = bf = work = work2 = rtw = nullptr;
+}
+
+template <class R>
+fgc_status DftPlanT<R>::run(int dir, DftResultT<R>& res, cudaStream_t s) {
+  switch (kind) {
+    case DftKind::Direct:
+      if (batch) {
+        k_direct_dft<R><<<batch, 64, 0, s>>>(work, work2, Lc, dir > 0 ? 1 : -1);
+        FGC_LAUNCHED(1);
+      }
+      res = DftResultT<R>{work2, Lc, 0, 0};
+      return FGC_OK;
+    case DftKind::Pow2:
+      FGC_TRY(pow2_rec<R>(work, batch, P, tw, P, dir, s));
+      res = DftResultT<R>{work, P, dir < 0 ? 1 : 0, 0};
+      return FGC_OK;
+    case DftKind::Bluestein: {
+      FGC_TRY(pow2_rec<R>(work, batch, P, tw, P, -1, s));
+      const uint64_t total = (uint64_t)batch * P;
+      if (total) {
+        k_pointwise_mul<T2><<<ceil_div(total, 256), 256, 0, s>>>(work, bf, P, total);
+        FGC_LAUNCHED(1);
+      }
+      FGC_TRY(pow2_rec<R>(work, batch, P, tw, P, +1, s));
+      res = DftResultT<R>{work, P, 0, 1};
+      return FGC_OK;
+    }
+  }
+  return FGC_ERR_INVALID;
+}
+
+template struct DftPlanT<float>;
+template struct DftPlanT<double>;
+
+}  // namespace fgc

@@ -1,0 +1,170 @@
+// Host-side internal interfaces between the plan (plan.cpp) and the kernel
+// translation units.  Not part of the public C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "fgc_types.h"
+#include "../../include/fgc_b200.h"
+
+namespace fgc {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+const std::string& last_error();
+fgc_status cuda_check(cudaError_t e, const char* what);
+void count_launch(uint64_t n = 1);
+#define FGC_CUDA(call)                                                  \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) return ::fgc::cuda_check(e_, #call);         \
+  } while (0)
+#define FGC_LAUNCHED(n)                                                 \
+  do {                                                                  \
+    ::fgc::count_launch(n);                                             \
+    cudaError_t e_ = cudaGetLastError();                                \
+    if (e_ != cudaSuccess) return ::fgc::cuda_check(e_, "kernel launch"); \
+  } while (0)
+#define FGC_TRY(expr)                                                   \
+  do {                                                                  \
+    fgc_status s_ = (expr);                                             \
+    if (s_ != FGC_OK) return s_;                                        \
+  } while (0)
+
+// ---------------------------------------------------------------- generic DFT
+// Complex DFT of length Lc for a batch of signals (fft_generic.cu), in
+// float32 (codec tails) or float64 (whole-signal primitives, calibrate).
+enum class DftKind : int { Direct = 0, Pow2 = 1, Bluestein = 2 };
+
+template <class R> struct Vec2;
+template <> struct Vec2<float> { using T = float2; };
+template <> struct Vec2<double> { using T = double2; };
+
+// Points one CTA transforms in shared memory (two 64 KB ping-pong halves).
+__host__ __device__ inline uint32_t smem_points(uint32_t real_bytes) { return real_bytes == 4 ? 4096u : 2048u; }
+
+__host__ __device__ inline void fft_split(uint32_t P, uint32_t cap, uint32_t& Rr, uint32_t& C) {
+  uint32_t lg = 0;
+  while ((1u << lg) < P) ++lg;
+  uint32_t lr = lg / 2;
+  while ((1u << lr) > cap) --lr;
+  Rr = 1u << lr;
+  C = P / Rr;
+}
+
+// Position of frequency k in the four-step engine layout of a size-P pow2
+// transform (natural when P fits one CTA).
+__host__ __device__ inline uint64_t engine_pos(uint32_t P, uint32_t cap, uint64_t k) {
+  uint64_t base = 0;
+  while (P > cap) {
+    uint32_t Rr, C;
+    fft_split(P, cap, Rr, C);
+    base += (k % Rr) * C;
+    k /= Rr;
+    P = C;
+  }
+  return base + k;
+}
+
+template <class R>
+struct DftResultT {
+  const typename Vec2<R>::T* base;  // buffer
+  uint64_t stride;                  // per batch item
+  int layout;                       // 0 natural, 1 engine layout
+  int chirp;                        // 1: multiply by chirp[k] / P (Bluestein)
+};
+
+template <class R>
+struct DftPlanT {
+  using T2 = typename Vec2<R>::T;
+  DftKind kind = DftKind::Direct;
+  uint32_t Lc = 1;        // DFT length
+  uint32_t P = 1;         // pow2 transform size (Pow2 / Bluestein); Lc for Direct
+  uint32_t batch = 0;
+  T2* tw = nullptr;       // P twiddles exp(-2 pi i j / P)
+  T2* chirp = nullptr;    // Bluestein chirp exp(-i pi n^2 / Lc), n < Lc
+  T2* bf = nullptr;       // Bluestein kernel spectrum, engine layout
+  T2* work = nullptr;     // batch * P
+  T2* work2 = nullptr;    // Direct output buffer
+  T2* rtw = nullptr;      // real-signal twiddles exp(-2 pi i k / L), k <= L/2 (even L)
+  fgc_status init(uint32_t Lc, uint32_t batch, cudaStream_t s);
+  void free_all();
+  // dir=-1 forward (natural input in work), dir=+1 unscaled inverse (Pow2:
+  // engine-layout input).  Bluestein always runs the forward chirp-z on the
+  // chirped, zero-padded input; inverse callers conjugate around it.
+  fgc_status run(int dir, DftResultT<R>& res, cudaStream_t s);
+};
+
+// Real-signal transforms of a batch of equal-length chunks described by
+// ChunkInfo entries [first, first+count) (real_fft.cu).
+template <class R>
+struct RealClassT {
+  uint32_t L = 0, bins = 0, first = 0, count = 0;
+  bool fused = false;
+  DftPlanT<R> dft;
+  fgc_status init(cudaStream_t s);   // needs L, count
+  void free_all() { dft.free_all(); }
+};
+
+// in_dtype: FGC_DTYPE_F32 / F64 input; spectrum and out in precision R.
+template <class R>
+fgc_status real_forward(RealClassT<R>& rc, const ChunkInfo* d_chunks, const void* in, int in_dtype, int half_pass,
+                        uint32_t* flags, typename Vec2<R>::T* spectrum, cudaStream_t s);
+template <class R>
+fgc_status real_inverse(RealClassT<R>& rc, const ChunkInfo* d_chunks, const typename Vec2<R>::T* spectrum, R* out,
+                        cudaStream_t s);
+
+// ---------------------------------------------------------------- codec kernels
+
+// Select (count mode) + quantize + pack from a chunk-major spectrum.
+// Chunks [first, first+count).  coeff_f64: spectrum is double2.
+fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_t count, const void* spectrum,
+                              int coeff_f64, const QuantParams& q, uint8_t* message, uint8_t* kept_mask,
+                              uint32_t* flags, cudaStream_t s);
+
+// Decode + weighted accumulate of W messages into a chunk-major spectrum.
+struct Weights {
+  float w[FGC_MAX_WORKERS];
+};
+fgc_status launch_decode_accumulate(const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                                    const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
+                                    const QuantParams& q, float2* spectrum, uint32_t max_slots, cudaStream_t s);
+
+// Wire format kernels (wire.cu).
+fgc_status launch_serialize(const ChunkInfo* d_chunks, uint32_t n_chunks, const uint8_t* message, int n_bits,
+                            const uint8_t header[FGC_HEADER_BYTES], uint8_t* wire, uint64_t* wire_len,
+                            uint64_t* scratch, cudaStream_t s);
+fgc_status launch_deserialize(const ChunkInfo* d_chunks, uint32_t n_chunks, const uint8_t* wire,
+                              const uint64_t* chunk_offsets, int n_bits, uint8_t* message, uint32_t* popcounts,
+                              cudaStream_t s);
+fgc_status launch_message_counts(const ChunkInfo* d_chunks, uint32_t n_chunks, const uint8_t* message, uint32_t* nnz,
+                                 cudaStream_t s);
+fgc_status launch_message_unpack(const ChunkInfo* d_chunks, uint32_t n_chunks, const uint8_t* message, int n_bits,
+                                 const uint64_t* code_offsets, uint8_t* flags01, uint32_t* codes, cudaStream_t s);
+fgc_status launch_message_pack(const ChunkInfo* d_chunks, uint32_t n_chunks, const uint8_t* flags01,
+                               const uint32_t* codes, const uint64_t* code_offsets, int n_bits, uint8_t* message,
+                               uint32_t* popcounts, uint32_t* flags, cudaStream_t s);
+fgc_status launch_scan_u64(uint64_t* v, uint32_t n, uint64_t* total, uint64_t add, cudaStream_t s);
+
+// Fused sm_100a kernels for 65536-sample chunks (fused.cu).
+struct FusedTables;
+bool fused_available();
+fgc_status fused_tables_init(FusedTables** t, cudaStream_t s);
+void fused_tables_free(FusedTables* t);
+fgc_status launch_fused_compress(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                                 const void* grad, int dtype, int half_pass, const QuantParams& q, uint8_t* message,
+                                 uint32_t* flags, cudaStream_t s);
+fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                               const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
+                               const QuantParams& q, float* out, cudaStream_t s);
+// Debug hooks: the fused kernels' own forward coefficients / inverse.
+fgc_status launch_fused_spectrum(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                                 const void* grad, int dtype, int half_pass, float2* spectrum, uint32_t* flags,
+                                 cudaStream_t s);
+fgc_status launch_fused_inverse(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                                const float2* spectrum, float* out, cudaStream_t s);
+
+}  // namespace fgc

@@ -1,0 +1,520 @@
+// The C ABI (include/fgc_b200.h): plans, the compress / decode-average hot
+// path, wire-format entry points.  Host logic only; kernels live in *.cu.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "fgc_internal.h"
+
+namespace fgc {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+fgc_status cuda_check(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return FGC_ERR_CUDA;
+}
+void count_launch(uint64_t n) { g_launches += n; }
+
+const std::string& last_error() { return g_last_error; }
+using RealClass = RealClassT<float>;
+
+static uint64_t a16(uint64_t x) { return (x + 15) & ~15ull; }
+
+}  // namespace fgc
+
+using namespace fgc;
+
+struct fgc_plan {
+  fgc_codec_desc desc{};
+  QuantParams q{};
+  uint32_t n_chunks = 0;
+  std::vector<ChunkInfo> chunks;
+  std::vector<RealClass> classes;
+  std::vector<uint64_t> seg_off, bin_off;
+  uint64_t msg_bytes = 0, spec_bins = 0, wire_max = 0, total_slots = 0;
+  uint32_t max_slots = 0;
+  ChunkInfo* d_chunks = nullptr;
+  float2* d_spec = nullptr;
+  uint64_t* d_scratch = nullptr;
+  FusedTables* fused = nullptr;
+  uint32_t fused_first = 0, fused_count = 0;     // chunk range taken by fused kernels
+};
+
+static QuantParams make_qparams(const fgc_codec_desc& d) {
+  QuantParams q{};
+  if (d.passthrough) {
+    q.n_bits = 32;
+    return q;
+  }
+  q.n_bits = d.quant.n_bits;
+  q.shift = 23 - d.quant.mantissa_bits;
+  q.pbase = d.quant.pbase;
+  q.npos = d.quant.pos_count;
+  q.nneg = d.quant.neg_count;
+  q.eps = d.quant.eps;
+  q.pos_cap = d.quant.max;
+  q.neg_cap = -d.quant.actual_min;
+  return q;
+}
+
+static bool fused_enabled() {
+  const char* e = getenv("FGC_DISABLE_FUSED");
+  return !(e && e[0] == '1');
+}
+
+extern "C" fgc_status fgc_message_layout(const fgc_codec_desc* d, uint32_t* n_chunks, uint64_t* message_bytes,
+                                         uint64_t* offs) {
+  if (!d || !n_chunks || !message_bytes) return FGC_ERR_INVALID;
+  if (d->n < 1 || d->chunk_size < 16 || !(d->theta >= 0.0 && d->theta <= 1.0)) {
+    set_error("invalid codec description");
+    return FGC_ERR_INVALID;
+  }
+  const int N = d->passthrough ? 32 : d->quant.n_bits;
+  const uint64_t full = d->n / d->chunk_size;
+  const uint64_t tail = d->n % d->chunk_size;
+  const uint64_t count = full + (tail ? 1 : 0);
+  uint64_t seg = 0;
+  for (uint64_t c = 0; c < count; ++c) {
+    const uint64_t L = c < full ? d->chunk_size : tail;
+    const uint64_t bins = L / 2 + 1, slots = 2 * bins;
+    uint64_t drop = (uint64_t)ceil(d->theta * (double)bins);
+    if (drop > bins) drop = bins;
+    const uint64_t maxnz = (d->mode == FGC_MODE_COUNT && !d->full_capacity) ? 2 * (bins - drop) : slots;
+    if (offs) offs[c] = seg;
+    seg += kSegHeader + a16(4 * ((slots + 31) / 32)) + a16(4 * ((maxnz * N + 31) / 32));
+  }
+  if (offs) offs[count] = seg;
+  *n_chunks = (uint32_t)count;
+  *message_bytes = seg;
+  return FGC_OK;
+}
+
+extern "C" fgc_status fgc_plan_create(const fgc_codec_desc* desc, fgc_plan** out) {
+  if (!desc || !out) { set_error("null argument"); return FGC_ERR_INVALID; }
+  *out = nullptr;
+  const fgc_codec_desc& d = *desc;
+  if (d.n < 1) { set_error("gradient must be a non-empty 1D sequence"); return FGC_ERR_INVALID; }
+  if (d.chunk_size < 16) { set_error("chunk_size must be >= 16"); return FGC_ERR_INVALID; }
+  if (!(d.theta >= 0.0 && d.theta <= 1.0)) { set_error("theta must be in [0, 1]"); return FGC_ERR_INVALID; }
+  if (d.mode != FGC_MODE_COUNT && d.mode != FGC_MODE_ENERGY) { set_error("unknown mode"); return FGC_ERR_INVALID; }
+  if (d.chunk_size > (1u << 20)) {
+    set_error("chunk_size above 2^20 is not supported by the GPU codec");
+    return FGC_ERR_UNSUPPORTED;
+  }
+  fgc_codec_desc dd = d;
+  if (!d.passthrough) {
+    fgc_status st = fgc_quantizer_validate(&dd.quant);
+    if (st != FGC_OK) return st;
+  }
+  fgc_plan* p = new fgc_plan();
+  p->desc = dd;
+  p->q = make_qparams(p->desc);
+  const int N = p->q.n_bits;
+  const uint64_t full = d.n / d.chunk_size;
+  const uint32_t tail = (uint32_t)(d.n % d.chunk_size);
+  p->n_chunks = (uint32_t)(full + (tail ? 1 : 0));
+  if (full) {
+    RealClass c;
+    c.L = d.chunk_size;
+    c.bins = c.L / 2 + 1;
+    c.first = 0;
+    c.count = (uint32_t)full;
+    c.fused = fused_available() && fused_enabled() && c.L == 65536 && d.mode == FGC_MODE_COUNT;
+    p->classes.push_back(c);
+  }
+  if (tail) {
+    RealClass c;
+    c.L = tail;
+    c.bins = tail / 2 + 1;
+    c.first = (uint32_t)full;
+    c.count = 1;
+    c.fused = false;
+    p->classes.push_back(c);
+  }
+  p->chunks.resize(p->n_chunks);
+  p->seg_off.resize(p->n_chunks + 1);
+  p->bin_off.resize(p->n_chunks + 1);
+  uint64_t seg = 0, bin = 0, slot = 0, in = 0;
+  for (uint32_t cls = 0; cls < p->classes.size(); ++cls) {
+    const RealClass& rc = p->classes[cls];
+    for (uint32_t j = 0; j < rc.count; ++j) {
+      const uint32_t c = rc.first + j;
+      ChunkInfo ci{};
+      ci.in_off = in;
+      ci.seg_off = seg;
+      ci.bin_off = bin;
+      ci.slot_off = slot;
+      ci.len = rc.L;
+      ci.bins = rc.bins;
+      ci.slots = 2 * rc.bins;
+      // k = ceil(theta * bins) in float64 (spectral.py:131)
+      const double kd = ceil(d.theta * (double)rc.bins);
+      ci.drop = (uint32_t)std::min<double>(kd, (double)rc.bins);
+      uint64_t maxnz = ci.slots;
+      if (d.mode == FGC_MODE_COUNT && !d.full_capacity) maxnz = 2ull * (rc.bins - ci.drop);
+      const uint64_t bm_words = (ci.slots + 31) / 32;
+      ci.code_off = (uint32_t)(kSegHeader + a16(4 * bm_words));
+      ci.code_cap = (uint32_t)((maxnz * N + 31) / 32);
+      ci.cls = cls;
+      ci.idx_in_cls = j;
+      p->chunks[c] = ci;
+      p->seg_off[c] = seg;
+      p->bin_off[c] = bin;
+      seg += ci.code_off + a16(4ull * ci.code_cap);
+      bin += ci.bins;
+      slot += ci.slots;
+      in += rc.L;
+      p->wire_max += 4 + (ci.slots + 7) / 8 + (maxnz * N + 7) / 8;
+      p->max_slots = std::max(p->max_slots, ci.slots);
+    }
+  }
+  p->seg_off[p->n_chunks] = seg;
+  p->bin_off[p->n_chunks] = bin;
+  p->msg_bytes = seg;
+  p->spec_bins = bin;
+  p->total_slots = slot;
+  p->wire_max += FGC_HEADER_BYTES;
+
+  auto fail = [&](fgc_status st) {
+    fgc_plan_destroy(p);
+    return st;
+  };
+  cudaStream_t s = 0;
+  cudaError_t e;
+  if ((e = cudaMalloc(&p->d_chunks, sizeof(ChunkInfo) * p->n_chunks)) != cudaSuccess) return fail(cuda_check(e, "cudaMalloc"));
+  if ((e = cudaMemcpy(p->d_chunks, p->chunks.data(), sizeof(ChunkInfo) * p->n_chunks, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return fail(cuda_check(e, "cudaMemcpy"));
+  if ((e = cudaMalloc(&p->d_spec, sizeof(float2) * p->spec_bins)) != cudaSuccess) return fail(cuda_check(e, "cudaMalloc"));
+  if ((e = cudaMalloc(&p->d_scratch, sizeof(uint64_t) * (p->n_chunks + 1))) != cudaSuccess)
+    return fail(cuda_check(e, "cudaMalloc"));
+  for (RealClass& rc : p->classes) {
+    if (rc.fused) {
+      fgc_status st = fused_tables_init(&p->fused, s);
+      if (st != FGC_OK) return fail(st);
+      p->fused_first = rc.first;
+      p->fused_count = rc.count;
+      continue;
+    }
+    fgc_status st = rc.init(s);
+    if (st != FGC_OK) return fail(st);
+  }
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(cuda_check(e, "plan init"));
+  *out = p;
+  return FGC_OK;
+}
+
+extern "C" void fgc_plan_destroy(fgc_plan* p) {
+  if (!p) return;
+  for (RealClass& rc : p->classes) rc.free_all();
+  if (p->fused) fused_tables_free(p->fused);
+  cudaFree(p->d_chunks);
+  cudaFree(p->d_spec);
+  cudaFree(p->d_scratch);
+  delete p;
+}
+
+extern "C" fgc_status fgc_plan_get_info(const fgc_plan* p, fgc_plan_info* out) {
+  if (!p || !out) return FGC_ERR_INVALID;
+  out->n = p->desc.n;
+  out->n_chunks = p->n_chunks;
+  out->chunk_size = p->desc.chunk_size;
+  out->tail_len = (uint32_t)(p->desc.n % p->desc.chunk_size);
+  out->n_bits = (uint32_t)p->q.n_bits;
+  out->message_bytes = p->msg_bytes;
+  out->wire_bytes_max = p->wire_max;
+  out->spectrum_bins = p->spec_bins;
+  out->fused_chunks = p->fused_count;
+  out->max_slots = p->max_slots;
+  out->total_slots = p->total_slots;
+  return FGC_OK;
+}
+
+extern "C" fgc_status fgc_plan_segment_offsets(const fgc_plan* p, uint64_t* o) {
+  if (!p || !o) return FGC_ERR_INVALID;
+  memcpy(o, p->seg_off.data(), sizeof(uint64_t) * (p->n_chunks + 1));
+  return FGC_OK;
+}
+
+extern "C" fgc_status fgc_plan_bin_offsets(const fgc_plan* p, uint64_t* o) {
+  if (!p || !o) return FGC_ERR_INVALID;
+  memcpy(o, p->bin_off.data(), sizeof(uint64_t) * (p->n_chunks + 1));
+  return FGC_OK;
+}
+
+// Forward transform of every non-fused class into `spectrum`.
+static fgc_status forward_generic(fgc_plan* p, const void* grad, int dtype, float2* spectrum, uint32_t* flags,
+                                  cudaStream_t s, bool include_fused_classes) {
+  for (RealClass& rc : p->classes) {
+    if (rc.fused && !include_fused_classes) continue;
+    if (rc.fused) {
+      set_error("fused class has no generic plan");
+      return FGC_ERR_UNSUPPORTED;
+    }
+    FGC_TRY(real_forward<float>(rc, p->d_chunks, grad, dtype, p->desc.half_pass, flags, spectrum, s));
+  }
+  return FGC_OK;
+}
+
+static fgc_status check_mode(const fgc_plan* p) {
+  if (p->desc.mode != FGC_MODE_COUNT) {
+    set_error("energy-mode selection is not implemented on the GPU yet");
+    return FGC_ERR_UNSUPPORTED;
+  }
+  return FGC_OK;
+}
+
+extern "C" fgc_status fgc_compress(fgc_plan* p, const void* grad, int dtype, uint8_t* message, uint32_t* flags,
+                                   void* stream) {
+  if (!p || !grad || !message || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_mode(p));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->fused_count)
+    FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, p->fused_first, p->fused_count, grad, dtype,
+                                  p->desc.half_pass, p->q, message, flags, s));
+  FGC_TRY(forward_generic(p, grad, dtype, p->d_spec, flags, s, false));
+  // generic chunks are the ones outside [fused_first, fused_first + fused_count)
+  for (RealClass& rc : p->classes) {
+    if (rc.fused) continue;
+    FGC_TRY(launch_select_pack(p->d_chunks, rc.first, rc.count, p->d_spec, 0, p->q, message, nullptr, flags, s));
+  }
+  return FGC_OK;
+}
+
+extern "C" fgc_status fgc_encode_spectrum(fgc_plan* p, const void* spectrum, uint8_t* message, uint8_t* kept_mask,
+                                          uint32_t* flags, void* stream) {
+  if (!p || !spectrum || !message || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_mode(p));
+  return launch_select_pack(p->d_chunks, 0, p->n_chunks, spectrum, 0, p->q, message, kept_mask, flags,
+                            static_cast<cudaStream_t>(stream));
+}
+
+extern "C" fgc_status fgc_forward_spectrum(fgc_plan* p, const void* grad, int dtype, void* spectrum, uint32_t* flags,
+                                           void* stream) {
+  if (!p || !grad || !spectrum || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (RealClass& rc : p->classes) {
+    if (!rc.fused) continue;
+    FGC_TRY(launch_fused_spectrum(p->fused, p->d_chunks, rc.first, rc.count, grad, dtype, p->desc.half_pass,
+                                  static_cast<float2*>(spectrum), flags, s));
+  }
+  return forward_generic(p, grad, dtype, static_cast<float2*>(spectrum), flags, s, false);
+}
+
+static fgc_status fill_weights(const double* weights, int W, Weights& w) {
+  if (W < 1 || W > FGC_MAX_WORKERS) {
+    set_error("worker count out of range");
+    return FGC_ERR_INVALID;
+  }
+  for (int i = 0; i < W; ++i) w.w[i] = weights ? (float)weights[i] : 1.0f;
+  return FGC_OK;
+}
+
+static fgc_status inverse_generic(fgc_plan* p, const float2* spectrum, float* out, cudaStream_t s) {
+  for (RealClass& rc : p->classes) {
+    if (rc.fused) continue;
+    FGC_TRY(real_inverse<float>(rc, p->d_chunks, spectrum, out, s));
+  }
+  return FGC_OK;
+}
+
+extern "C" fgc_status fgc_decode_average(fgc_plan* p, const uint8_t* messages, int W, uint64_t stride,
+                                         const double* weights, float* out, void* stream) {
+  if (!p || !messages || !out) { set_error("null argument"); return FGC_ERR_INVALID; }
+  Weights w;
+  FGC_TRY(fill_weights(weights, W, w));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->fused_count)
+    FGC_TRY(launch_fused_decode(p->fused, p->d_chunks, p->fused_first, p->fused_count, messages, W, stride, w, p->q,
+                                out, s));
+  for (RealClass& rc : p->classes) {
+    if (rc.fused) continue;
+    FGC_TRY(launch_decode_accumulate(p->d_chunks, rc.first, rc.count, messages, W, stride, w, p->q, p->d_spec,
+                                     p->max_slots, s));
+  }
+  return inverse_generic(p, p->d_spec, out, s);
+}
+
+extern "C" fgc_status fgc_decode_spectrum(fgc_plan* p, const uint8_t* messages, int W, uint64_t stride,
+                                          const double* weights, void* spectrum, void* stream) {
+  if (!p || !messages || !spectrum) { set_error("null argument"); return FGC_ERR_INVALID; }
+  Weights w;
+  FGC_TRY(fill_weights(weights, W, w));
+  return launch_decode_accumulate(p->d_chunks, 0, p->n_chunks, messages, W, stride, w, p->q,
+                                  static_cast<float2*>(spectrum), p->max_slots, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" fgc_status fgc_inverse_spectrum(fgc_plan* p, const void* spectrum, float* out, void* stream) {
+  if (!p || !spectrum || !out) { set_error("null argument"); return FGC_ERR_INVALID; }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (RealClass& rc : p->classes) {
+    if (!rc.fused) continue;
+    FGC_TRY(launch_fused_inverse(p->fused, p->d_chunks, rc.first, rc.count, static_cast<const float2*>(spectrum),
+                                 out, s));
+  }
+  return inverse_generic(p, static_cast<const float2*>(spectrum), out, s);
+}
+
+// ------------------------------------------------------------------ wire
+
+static void build_header(const fgc_plan* p, uint8_t h[FGC_HEADER_BYTES]) {
+  const fgc_codec_desc& d = p->desc;
+  uint8_t flags = 0;
+  if (d.half_pass) flags |= 1;
+  if (d.mode == FGC_MODE_ENERGY) flags |= 2;
+  if (d.passthrough) flags |= 4;
+  const float theta = (float)d.theta;
+  const float qmin = d.passthrough ? 0.0f : d.quant.min;
+  const float qmax = d.passthrough ? 0.0f : d.quant.max;
+  const float qeps = d.passthrough ? 0.0f : d.quant.eps;
+  const uint8_t nb = d.passthrough ? 32 : (uint8_t)d.quant.n_bits;
+  const uint8_t mb = d.passthrough ? 0 : (uint8_t)d.quant.mantissa_bits;
+  memcpy(h, "FGC1", 4);
+  h[4] = 1;
+  h[5] = flags;
+  memcpy(h + 6, &d.n, 8);
+  memcpy(h + 14, &d.chunk_size, 4);
+  memcpy(h + 18, &theta, 4);
+  memcpy(h + 22, &qmin, 4);
+  memcpy(h + 26, &qmax, 4);
+  memcpy(h + 30, &qeps, 4);
+  h[34] = nb;
+  h[35] = mb;
+}
+
+extern "C" fgc_status fgc_serialize(fgc_plan* p, const uint8_t* message, uint8_t* wire, uint64_t* wire_len,
+                                    void* stream) {
+  if (!p || !message || !wire || !wire_len) { set_error("null argument"); return FGC_ERR_INVALID; }
+  uint8_t h[FGC_HEADER_BYTES];
+  build_header(p, h);
+  return launch_serialize(p->d_chunks, p->n_chunks, message, p->q.n_bits, h, wire, wire_len, p->d_scratch,
+                          static_cast<cudaStream_t>(stream));
+}
+
+extern "C" fgc_status fgc_parse_header(const uint8_t* w, uint64_t len, fgc_codec_desc* d) {
+  if (!w || !d) return FGC_ERR_INVALID;
+  if (len < FGC_HEADER_BYTES) { set_error("buffer is shorter than the header"); return FGC_ERR_TRUNCATED; }
+  if (memcmp(w, "FGC1", 4) != 0) { set_error("bad magic"); return FGC_ERR_HEADER; }
+  if (w[4] != 1) { set_error("unsupported version"); return FGC_ERR_HEADER; }
+  const uint8_t flags = w[5];
+  if (flags & ~0x07) { set_error("unknown flag bits"); return FGC_ERR_HEADER; }
+  uint64_t n;
+  uint32_t chunk;
+  float theta, qmin, qmax, qeps;
+  memcpy(&n, w + 6, 8);
+  memcpy(&chunk, w + 14, 4);
+  memcpy(&theta, w + 18, 4);
+  memcpy(&qmin, w + 22, 4);
+  memcpy(&qmax, w + 26, 4);
+  memcpy(&qeps, w + 30, 4);
+  const int nb = w[34], mb = w[35];
+  if (n < 1) { set_error("original_len must be >= 1"); return FGC_ERR_HEADER; }
+  if (chunk < 16) { set_error("chunk_size below minimum 16"); return FGC_ERR_HEADER; }
+  if (!(isfinite(theta) && theta >= 0.0f && theta <= 1.0f)) { set_error("theta outside [0, 1]"); return FGC_ERR_HEADER; }
+  memset(d, 0, sizeof(*d));
+  d->n = n;
+  d->chunk_size = chunk;
+  d->theta = (double)theta;
+  d->mode = (flags & 2) ? FGC_MODE_ENERGY : FGC_MODE_COUNT;
+  d->half_pass = (flags & 1) ? 1 : 0;
+  d->passthrough = (flags & 4) ? 1 : 0;
+  if (d->passthrough) {
+    if (nb != 32) { set_error("passthrough flag requires N=32"); return FGC_ERR_HEADER; }
+  } else {
+    fgc_status st = fgc_quantizer_from_params(qmin, qmax, nb, mb, qeps, &d->quant);
+    if (st != FGC_OK) {
+      set_error("invalid quantizer parameters: " + last_error());
+      return FGC_ERR_HEADER;
+    }
+  }
+  return FGC_OK;
+}
+
+extern "C" fgc_status fgc_wire_index(const uint8_t* w, uint64_t len, const fgc_codec_desc* d, uint64_t* offsets,
+                                     uint32_t* nnz, uint32_t* n_valid) {
+  if (!w || !d || !offsets || !nnz || !n_valid) return FGC_ERR_INVALID;
+  const int N = d->passthrough ? 32 : d->quant.n_bits;
+  uint64_t pos = FGC_HEADER_BYTES;
+  const uint64_t full = d->n / d->chunk_size;
+  const uint64_t tail = d->n % d->chunk_size;
+  const uint64_t count = full + (tail ? 1 : 0);
+  *n_valid = 0;
+  for (uint64_t c = 0; c < count; ++c) {
+    const uint64_t L = c < full ? d->chunk_size : tail;
+    const uint64_t slots = 2 * (L / 2 + 1);
+    if (pos + 4 > len) { set_error("buffer ended before chunk header"); return FGC_ERR_TRUNCATED; }
+    uint32_t k;
+    memcpy(&k, w + pos, 4);
+    offsets[c] = pos;
+    nnz[c] = k;
+    pos += 4;
+    const uint64_t bmb = (slots + 7) / 8;
+    if (pos + bmb > len) { set_error("buffer ended inside the bitmap"); return FGC_ERR_TRUNCATED; }
+    pos += bmb;
+    const uint64_t cb = ((uint64_t)k * N + 7) / 8;
+    if (pos + cb > len) {
+      *n_valid = (uint32_t)c;   // bitmap of chunk c is present; its codes are not
+      set_error("buffer ended inside the packed codes");
+      return FGC_ERR_TRUNCATED;
+    }
+    pos += cb;
+    *n_valid = (uint32_t)(c + 1);
+  }
+  if (pos != len) {
+    set_error(std::to_string(len - pos) + " unexpected trailing bytes");
+    return FGC_ERR_FORMAT;
+  }
+  return FGC_OK;
+}
+
+extern "C" fgc_status fgc_deserialize(fgc_plan* p, const uint8_t* wire, const uint64_t* chunk_offsets,
+                                      uint8_t* message, uint32_t* popcounts, void* stream) {
+  if (!p || !wire || !chunk_offsets || !message || !popcounts) { set_error("null argument"); return FGC_ERR_INVALID; }
+  return launch_deserialize(p->d_chunks, p->n_chunks, wire, chunk_offsets, p->q.n_bits, message, popcounts,
+                            static_cast<cudaStream_t>(stream));
+}
+
+extern "C" fgc_status fgc_message_counts(fgc_plan* p, const uint8_t* message, uint32_t* nnz, void* stream) {
+  if (!p || !message || !nnz) return FGC_ERR_INVALID;
+  return launch_message_counts(p->d_chunks, p->n_chunks, message, nnz, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" fgc_status fgc_message_unpack(fgc_plan* p, const uint8_t* message, const uint64_t* code_offsets,
+                                         uint8_t* flags01, uint32_t* codes, void* stream) {
+  if (!p || !message || !code_offsets || !flags01 || !codes) return FGC_ERR_INVALID;
+  return launch_message_unpack(p->d_chunks, p->n_chunks, message, p->q.n_bits, code_offsets, flags01, codes,
+                               static_cast<cudaStream_t>(stream));
+}
+
+extern "C" fgc_status fgc_message_pack(fgc_plan* p, const uint8_t* flags01, const uint32_t* codes,
+                                       const uint64_t* code_offsets, uint8_t* message, uint32_t* popcounts,
+                                       uint32_t* flags, void* stream) {
+  if (!p || !flags01 || !code_offsets || !message || !popcounts || !flags) return FGC_ERR_INVALID;
+  return launch_message_pack(p->d_chunks, p->n_chunks, flags01, codes, code_offsets, p->q.n_bits, message,
+                             popcounts, flags, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" fgc_status fgc_allgather_average(fgc_plan* p, void* comm, int nranks, const void* grad, int dtype,
+                                            const double* weights, uint8_t* message, uint8_t* gathered, float* out,
+                                            uint32_t* flags, void* stream) {
+  if (!p || !grad || !message || !out || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(fgc_compress(p, grad, dtype, message, flags, stream));
+  if (nranks > 1) {
+    if (!comm || !gathered) { set_error("multi-rank average needs a communicator and a gather buffer"); return FGC_ERR_INVALID; }
+    FGC_TRY(fgc_allgather(comm, message, gathered, p->msg_bytes, stream));
+    return fgc_decode_average(p, gathered, nranks, p->msg_bytes, weights, out, stream);
+  }
+  return fgc_decode_average(p, message, 1, p->msg_bytes, weights, out, stream);
+}
+
+extern "C" const char* fgc_last_error(void) { return g_last_error.c_str(); }
+extern "C" int fgc_version(void) { return 0x000100; }
+extern "C" uint64_t fgc_kernel_launches(void) { return g_launches.load(); }

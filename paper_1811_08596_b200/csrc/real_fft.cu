@@ -1,0 +1,290 @@
+// Real-signal glue around the generic complex DFT engine (fft_generic.cu):
+// numpy's rfft / irfft semantics (spectral.py:88-106) for a batch of equal
+// length chunks, in float32 (codec) or float64 (primitives).
+//
+//   even L: z[n] = x[2n] + i x[2n+1], Z = DFT_{L/2}(z),
+//           X[k] = (Z[k] + conj Z[L/2-k])/2 - i W_L^k (Z[k] - conj Z[L/2-k])/2
+//   odd  L: Z = DFT_L(x + 0i), X[k] = Z[k]
+//   inverse: the algebraic inverse of the above; Im X[0] (and Im X[L/2] for
+//   even L) are ignored exactly like numpy's irfft.
+// The forward load applies the codec's input checks: non-finite values
+// (codec.py:225-226) and the optional binary16 round trip with overflow
+// detection (spectral.py:189-196, codec.py:211-214).
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <math.h>
+
+#include "fgc_device.cuh"
+#include "fgc_internal.h"
+
+namespace fgc {
+
+namespace {
+
+inline uint32_t cdiv(uint64_t a, uint32_t b) { return (uint32_t)((a + b - 1) / b); }
+
+__device__ __forceinline__ float2 mk2(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ double2 mk2(double x, double y) { return make_double2(x, y); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return cmul(a, b); }
+__device__ __forceinline__ double2 mul2(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+template <class T2> __device__ __forceinline__ T2 cj(T2 a) { return mk2(a.x, -a.y); }
+
+// ------------------------------------------------------------- input loads
+
+template <class R, class In> struct Loader;
+template <> struct Loader<float, float> {
+  __device__ static float get(const float* g, uint64_t i, int half, uint32_t* flags) {
+    float x = g[i];
+    if (!isfinite(x)) { atomicOr(flags, FGC_FLAG_NONFINITE); return 0.0f; }
+    if (half) {
+      x = __half2float(__float2half_rn(x));
+      if (isinf(x)) atomicOr(flags, FGC_FLAG_HALF_OVERFLOW);
+    }
+    return x;
+  }
+};
+template <> struct Loader<float, double> {
+  __device__ static float get(const double* g, uint64_t i, int half, uint32_t* flags) {
+    const double d = g[i];
+    if (!isfinite(d)) { atomicOr(flags, FGC_FLAG_NONFINITE); return 0.0f; }
+    float x;
+    if (half) {
+      x = __half2float(__double2half(d));     // f64 -> f16 directly, like numpy
+      if (isinf(x)) atomicOr(flags, FGC_FLAG_HALF_OVERFLOW);
+    } else {
+      x = (float)d;
+      if (isinf(x)) atomicOr(flags, FGC_FLAG_F32_RANGE);
+    }
+    return x;
+  }
+};
+template <> struct Loader<double, double> {
+  __device__ static double get(const double* g, uint64_t i, int, uint32_t* flags) {
+    const double d = g[i];
+    if (!isfinite(d)) { atomicOr(flags, FGC_FLAG_NONFINITE); return 0.0; }
+    return d;
+  }
+};
+template <> struct Loader<double, float> {
+  __device__ static double get(const float* g, uint64_t i, int, uint32_t* flags) {
+    const float x = g[i];
+    if (!isfinite(x)) { atomicOr(flags, FGC_FLAG_NONFINITE); return 0.0; }
+    return (double)x;
+  }
+};
+
+template <class R>
+struct Args {
+  using T2 = typename Vec2<R>::T;
+  const ChunkInfo* chunks;
+  uint32_t first, L, Lc, Pw, P, bins, cap;
+  int kind;
+  T2* work;
+  const T2* chirp;
+  const T2* rtw;
+  R invP;
+};
+
+template <class R, class In>
+__global__ void k_prep(Args<R> a, const In* in, int half, uint32_t* flags) {
+  using T2 = typename Vec2<R>::T;
+  const uint32_t j = blockIdx.y;
+  const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.Pw) return;
+  const ChunkInfo ci = a.chunks[a.first + j];
+  T2 v = mk2((R)0, (R)0);
+  if (n < a.Lc) {
+    if ((a.L & 1u) == 0) {
+      v.x = Loader<R, In>::get(in, ci.in_off + 2ull * n, half, flags);
+      v.y = Loader<R, In>::get(in, ci.in_off + 2ull * n + 1, half, flags);
+    } else {
+      v.x = Loader<R, In>::get(in, ci.in_off + n, half, flags);
+    }
+    if (a.kind == (int)DftKind::Bluestein) v = mul2(v, a.chirp[n]);
+  }
+  a.work[(uint64_t)j * a.Pw + n] = v;
+}
+
+template <class R>
+struct Res {
+  const typename Vec2<R>::T* base;
+  uint64_t stride;
+  int layout, chirp;
+};
+
+template <class R>
+__device__ __forceinline__ typename Vec2<R>::T res_get(const Args<R>& a, const Res<R>& r, uint32_t j, uint64_t k) {
+  const uint64_t pos = r.layout ? engine_pos(a.P, a.cap, k) : k;
+  typename Vec2<R>::T v = r.base[(uint64_t)j * r.stride + pos];
+  if (r.chirp) {
+    v = mul2(v, a.chirp[k]);
+    v.x *= a.invP;
+    v.y *= a.invP;
+  }
+  return v;
+}
+
+template <class R>
+__global__ void k_post(Args<R> a, Res<R> r, typename Vec2<R>::T* spectrum) {
+  using T2 = typename Vec2<R>::T;
+  const uint32_t j = blockIdx.y;
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= a.bins) return;
+  const ChunkInfo ci = a.chunks[a.first + j];
+  T2 X;
+  if ((a.L & 1u) == 0) {
+    const uint32_t Lc = a.Lc;
+    const T2 zk = res_get(a, r, j, k == Lc ? 0 : k);
+    const T2 zm = res_get(a, r, j, k == 0 ? 0 : Lc - k);
+    const T2 A = mk2(zk.x + zm.x, zk.y - zm.y);   // Z[k] + conj Z[Lc-k]
+    const T2 B = mk2(zk.x - zm.x, zk.y + zm.y);   // Z[k] - conj Z[Lc-k]
+    const T2 t = mul2(a.rtw[k], mk2(B.y, -B.x));  // W^k (-i B)
+    X = mk2((R)0.5 * (A.x + t.x), (R)0.5 * (A.y + t.y));
+    if (k == 0 || k == Lc) X.y = (R)0;
+  } else {
+    X = res_get(a, r, j, k);
+    if (k == 0) X.y = (R)0;
+  }
+  spectrum[ci.bin_off + k] = X;
+}
+
+template <class R>
+__global__ void k_iprep(Args<R> a, const typename Vec2<R>::T* spectrum) {
+  using T2 = typename Vec2<R>::T;
+  const uint32_t j = blockIdx.y;
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= a.Pw) return;
+  const ChunkInfo ci = a.chunks[a.first + j];
+  const T2* X = spectrum + ci.bin_off;
+  T2 Z = mk2((R)0, (R)0);
+  if (k < a.Lc) {
+    if ((a.L & 1u) == 0) {
+      const uint32_t Lc = a.Lc;
+      T2 xk = X[k], xm = X[Lc - k];
+      if (k == 0) { xk.y = (R)0; xm.y = (R)0; }   // DC and Nyquist imag ignored
+      const T2 E = mk2((R)0.5 * (xk.x + xm.x), (R)0.5 * (xk.y - xm.y));
+      const T2 D = mk2((R)0.5 * (xk.x - xm.x), (R)0.5 * (xk.y + xm.y));
+      const T2 O = mul2(D, cj(a.rtw[k]));         // W^{-k} D
+      Z = mk2(E.x - O.y, E.y + O.x);              // E + i O
+    } else {
+      const uint32_t h = (a.L - 1) / 2;
+      if (k <= h) {
+        Z = X[k];
+        if (k == 0) Z.y = (R)0;
+      } else {
+        Z = cj(X[a.L - k]);
+      }
+    }
+  }
+  uint64_t pos = k;
+  if (a.kind == (int)DftKind::Bluestein) {
+    if (k < a.Lc) Z = mul2(cj(Z), a.chirp[k]);
+  } else if (a.kind == (int)DftKind::Pow2) {
+    pos = engine_pos(a.P, a.cap, k);
+  }
+  a.work[(uint64_t)j * a.Pw + pos] = Z;
+}
+
+template <class R>
+__global__ void k_ipost(Args<R> a, Res<R> r, R* out, R scale) {
+  using T2 = typename Vec2<R>::T;
+  const uint32_t j = blockIdx.y;
+  const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.Lc) return;
+  const ChunkInfo ci = a.chunks[a.first + j];
+  T2 v = res_get(a, r, j, n);
+  if (a.kind == (int)DftKind::Bluestein) v = cj(v);
+  if ((a.L & 1u) == 0) {
+    out[ci.in_off + 2ull * n] = v.x * scale;
+    out[ci.in_off + 2ull * n + 1] = v.y * scale;
+  } else {
+    out[ci.in_off + n] = v.x * scale;
+  }
+}
+
+template <class R>
+Args<R> make_args(const RealClassT<R>& rc, const ChunkInfo* d_chunks) {
+  Args<R> a;
+  const DftPlanT<R>& d = rc.dft;
+  a.chunks = d_chunks;
+  a.first = rc.first;
+  a.L = rc.L;
+  a.Lc = d.Lc;
+  a.Pw = d.P;
+  a.P = d.P;
+  a.bins = rc.bins;
+  a.cap = smem_points(sizeof(R));
+  a.kind = (int)d.kind;
+  a.work = d.work;
+  a.chirp = d.chirp;
+  a.rtw = d.rtw;
+  a.invP = (R)1 / (R)d.P;
+  return a;
+}
+
+}  // namespace
+
+template <class R>
+fgc_status RealClassT<R>::init(cudaStream_t s) {
+  using T2 = typename Vec2<R>::T;
+  const uint32_t Lc = (L % 2 == 0) ? L / 2 : L;
+  FGC_TRY(dft.init(Lc, count, s));
+  if (L % 2 == 0) {
+    std::vector<T2> h(Lc + 1);
+    for (uint32_t k = 0; k <= Lc; ++k) {
+      const double ang = -2.0 * M_PI * (double)k / (double)L;
+      h[k].x = (R)cos(ang);
+      h[k].y = (R)sin(ang);
+    }
+    FGC_CUDA(cudaMalloc(&dft.rtw, sizeof(T2) * (Lc + 1)));
+    FGC_CUDA(cudaMemcpy(dft.rtw, h.data(), sizeof(T2) * (Lc + 1), cudaMemcpyHostToDevice));
+  }
+  return FGC_OK;
+}
+
+template <class R>
+fgc_status real_forward(RealClassT<R>& rc, const ChunkInfo* d_chunks, const void* in, int in_dtype, int half_pass,
+                        uint32_t* flags, typename Vec2<R>::T* spectrum, cudaStream_t s) {
+  if (!rc.count) return FGC_OK;
+  Args<R> a = make_args(rc, d_chunks);
+  dim3 grid(cdiv(a.Pw, 256), rc.count);
+  if (in_dtype == FGC_DTYPE_F64)
+    k_prep<R, double><<<grid, 256, 0, s>>>(a, static_cast<const double*>(in), half_pass, flags);
+  else
+    k_prep<R, float><<<grid, 256, 0, s>>>(a, static_cast<const float*>(in), half_pass, flags);
+  FGC_LAUNCHED(1);
+  DftResultT<R> r;
+  FGC_TRY(rc.dft.run(-1, r, s));
+  Res<R> rr{r.base, r.stride, r.layout, r.chirp};
+  k_post<R><<<dim3(cdiv(a.bins, 256), rc.count), 256, 0, s>>>(a, rr, spectrum);
+  FGC_LAUNCHED(1);
+  return FGC_OK;
+}
+
+template <class R>
+fgc_status real_inverse(RealClassT<R>& rc, const ChunkInfo* d_chunks, const typename Vec2<R>::T* spectrum, R* out,
+                        cudaStream_t s) {
+  if (!rc.count) return FGC_OK;
+  Args<R> a = make_args(rc, d_chunks);
+  k_iprep<R><<<dim3(cdiv(a.Pw, 256), rc.count), 256, 0, s>>>(a, spectrum);
+  FGC_LAUNCHED(1);
+  DftResultT<R> r;
+  FGC_TRY(rc.dft.run(+1, r, s));
+  Res<R> rr{r.base, r.stride, r.layout, r.chirp};
+  k_ipost<R><<<dim3(cdiv(a.Lc, 256), rc.count), 256, 0, s>>>(a, rr, out, (R)1 / (R)a.Lc);
+  FGC_LAUNCHED(1);
+  return FGC_OK;
+}
+
+template struct RealClassT<float>;
+template struct RealClassT<double>;
+template fgc_status real_forward<float>(RealClassT<float>&, const ChunkInfo*, const void*, int, int, uint32_t*, float2*,
+                                        cudaStream_t);
+template fgc_status real_forward<double>(RealClassT<double>&, const ChunkInfo*, const void*, int, int, uint32_t*,
+                                         double2*, cudaStream_t);
+template fgc_status real_inverse<float>(RealClassT<float>&, const ChunkInfo*, const float2*, float*, cudaStream_t);
+template fgc_status real_inverse<double>(RealClassT<double>&, const ChunkInfo*, const double2*, double*, cudaStream_t);
+
+}  // namespace fgc

@@ -1,0 +1,441 @@
+"""GPU parity tests: the CUDA path through the C ABI against the CPU oracle
+(oracle/, pinned to the reference) and the reference's golden vectors.
+
+Bars (SURVEY.md 8c / DESIGN.md "Parity"):
+  * bitmap, codes, kept mask: BIT-EXACT given identical coefficients
+    (stage injection);
+  * forward coefficients vs numpy's float64 rfft: max error <= 2e-6 x the
+    chunk's coefficient RMS-scale (fp32 FFT);
+  * decoded / averaged gradients vs the oracle on the same message:
+    rel-L2 <= 1e-5;
+  * wire bytes: byte-exact round trips of the reference fixtures.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+F = pytest.importorskip("paper_1811_08596_b200")
+from paper_1811_08596_b200 import debug  # noqa: E402
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def lat_of(q):
+    return None if q is None else O.lattice(q.min, q.max, q.n_bits, q.mantissa_bits, q.eps)
+
+
+def q_of(rec):
+    if rec is None:
+        return None
+    return F.QuantizerConfig.from_params(rec["min"], rec["max"], rec["n_bits"], rec["mantissa_bits"], rec["eps"])
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb else 1.0)
+
+
+def segments_valid_bytes(dev: bytes, n, chunk, theta, width):
+    """Per chunk: nnz, wire bitmap bytes, wire code bytes from a device message."""
+    layout, _ = O.device_layout(n, chunk, theta, width)
+    out = []
+    for (off, bmo, co, cap), L in zip(layout, O.chunk_lengths(n, chunk)):
+        nnz = int.from_bytes(dev[off:off + 4], "little")
+        bmb = (O.slot_count(L) + 7) // 8
+        cb = (nnz * width + 7) // 8
+        out.append((nnz, dev[off + bmo:off + bmo + bmb], dev[off + co:off + co + cb]))
+    return out
+
+
+# ---------------------------------------------------------------- injection
+
+def test_injection_golden_vectors(golden):
+    meta, arr = golden
+    for rec in meta["injection"]:
+        L, theta = rec["length"], rec["theta"]
+        q = q_of(rec["quantizer"])
+        cfg = F.CodecConfig(F.SparsificationSpec(theta), q, chunk_size=max(16, L))
+        coeffs = arr[rec["key"] + "_coeffs"]
+        msg, mask = debug.encode_spectrum(coeffs, L, cfg)
+        np.testing.assert_array_equal(mask, arr[rec["key"] + "_mask"], err_msg=rec["key"])
+        width = 32 if q is None else q.n_bits
+        (nnz, bm, cb), = segments_valid_bytes(debug.message_bytes(msg), L, max(16, L), theta, width)
+        assert nnz == rec["kept"], rec["key"]
+        assert bm.hex() == rec["bitmap_hex"], rec["key"]
+        assert cb.hex() == rec["codes_hex"], rec["key"]
+
+
+def _random_spectrum(rng, n, chunk, ties=True):
+    bins = [L // 2 + 1 for L in O.chunk_lengths(n, chunk)]
+    parts = []
+    for b in bins:
+        scale = np.exp(rng.uniform(-3, 3))
+        c = (rng.standard_normal(b) + 1j * rng.standard_normal(b)) * scale
+        c[0] = c[0].real
+        if ties:
+            c[5::97] = c[5]                 # exact magnitude ties
+            c[7::131] = np.conj(c[7])       # conjugate twins: equal key
+            c[11::53] = 0                   # zeros
+            c[13::211] = c[13] * 1e-30      # tiny values
+        parts.append(c.astype(np.complex64))
+    return np.concatenate(parts)
+
+
+@pytest.mark.parametrize("theta", [0.0, 0.3, 0.9, 0.99, 1.0])
+@pytest.mark.parametrize("nm", [(8, 3), (4, 2), (6, 2), (16, 9), None])
+def test_injection_random_bit_exact(theta, nm):
+    rng = np.random.default_rng(int(theta * 100) + (0 if nm is None else nm[0]))
+    n, chunk = 300_000, 65536
+    spec = _random_spectrum(rng, n, chunk)
+    q = None if nm is None else F.tune_eps(-3.0 * np.abs(spec).max(), 3.0 * np.abs(spec).max(), *nm)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta), q, chunk_size=chunk)
+    msg, mask = debug.encode_spectrum(spec, n, cfg)
+    got = debug.message_bytes(msg)
+    lat = lat_of(q)
+    width = 32 if q is None else q.n_bits
+    pos = 0
+    gsegs = segments_valid_bytes(got, n, chunk, theta, width)
+    for L, (nnz, bm, cb) in zip(O.chunk_lengths(n, chunk), gsegs):
+        b = L // 2 + 1
+        kept, ch = O.encode_spectrum(spec[pos:pos + b], L, theta, "count", lat)
+        np.testing.assert_array_equal(mask[pos:pos + b], kept)
+        assert nnz == ch.codes.size
+        assert bm == O.flags_to_bytes(ch.bitmap)
+        assert cb == O.codes_to_bytes(ch.codes, width)
+        pos += b
+
+
+def test_injection_degenerate_chunks():
+    """All-equal magnitudes, all zeros and sub-2^-50 values force the exact
+    fallback selection; the stable index tie-break must still hold."""
+    n, chunk = 4 * 4096, 4096
+    b = chunk // 2 + 1
+    parts = [np.full(b, 1.5 + 0j), np.zeros(b), np.full(b, 3e-30 - 1e-30j),
+             np.where(np.arange(b) % 2 == 0, 1e-20 + 0j, 0j)]
+    spec = np.concatenate(parts).astype(np.complex64)
+    q = F.tune_eps(-10.0, 10.0, 8, 3)
+    for theta in (0.3, 0.5, 0.77):
+        cfg = F.CodecConfig(F.SparsificationSpec(theta), q, chunk_size=chunk)
+        _, mask = debug.encode_spectrum(spec, n, cfg)
+        for i in range(4):
+            kept, _ = O.encode_spectrum(spec[i * b:(i + 1) * b], chunk, theta, "count", lat_of(q))
+            np.testing.assert_array_equal(mask[i * b:(i + 1) * b], kept)
+
+
+# ---------------------------------------------------------------- FFTs
+
+@pytest.mark.parametrize("n,chunk", [(1_000_000, 65536), (65536 * 3, 65536), (40960 + 65536, 65536),
+                                     (5000, 1024), (777, 64), (100, 17), (33, 16), (65537, 65536)])
+def test_forward_coefficients_match_float64_rfft(n, chunk):
+    rng = np.random.default_rng(n)
+    g = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.9), F.tune_eps(-5, 5, 8, 3), chunk_size=chunk)
+    spec = debug.forward_spectrum(g, cfg)
+    pos = 0
+    off = 0
+    for L in O.chunk_lengths(n, chunk):
+        ref = np.fft.rfft(g[off:off + L].astype(np.float64))
+        got = spec[pos:pos + ref.size]
+        scale = np.sqrt(np.mean(np.abs(ref) ** 2)) + 1e-30
+        err = np.abs(got.astype(np.complex128) - ref).max() / scale
+        assert err <= 2e-6, (L, err)
+        assert got[0].imag == 0 and (L % 2 or got[-1].imag == 0)
+        pos += ref.size
+        off += L
+
+
+@pytest.mark.parametrize("n,chunk", [(1_000_000, 65536), (5000, 1024), (777, 64), (101, 17)])
+def test_inverse_matches_float64_irfft(n, chunk):
+    rng = np.random.default_rng(n + 1)
+    bins = [L // 2 + 1 for L in O.chunk_lengths(n, chunk)]
+    spec = np.concatenate([(rng.standard_normal(b) + 1j * rng.standard_normal(b)) for b in bins]).astype(np.complex64)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.9), None, chunk_size=chunk)
+    out = debug.inverse_spectrum(spec, n, cfg)
+    pos = off = 0
+    for L, b in zip(O.chunk_lengths(n, chunk), bins):
+        ref = np.fft.irfft(spec[pos:pos + b].astype(np.complex128), n=L)   # ignores Im of DC/Nyquist too
+        assert rel_l2(out[off:off + L], ref) <= 1e-6, L
+        pos += b
+        off += L
+
+
+# ---------------------------------------------------------------- decode
+
+@pytest.mark.parametrize("theta,nm", [(0.9, (8, 3)), (0.0, None), (0.5, (6, 2)), (0.99, (16, 9))])
+def test_decode_matches_oracle_on_same_message(theta, nm):
+    rng = np.random.default_rng(7)
+    n, chunk = 200_000, 65536
+    g = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+    q = None if nm is None else F.calibrate([g], *nm)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta), q, chunk_size=chunk)
+    msg = F.compress(g, cfg)
+    wire = F.serialize(msg)
+    ref = O.decompress(O.from_wire(wire))
+    got = F.decompress(msg)
+    assert got.dtype == np.float64
+    assert rel_l2(got, ref) <= 1e-5
+
+
+def test_compress_matches_oracle_given_gpu_coefficients():
+    """Full K1->K3: the GPU message equals the oracle's message built from
+    the GPU's own coefficients (bit-exact), and those coefficients match the
+    float64 rfft (test above)."""
+    rng = np.random.default_rng(8)
+    n, chunk = 1_000_000, 65536
+    g = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+    q = F.calibrate([g], 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.9), q, chunk_size=chunk)
+    spec = debug.forward_spectrum(g, cfg)
+    msg = F.compress(g, cfg)
+    got = segments_valid_bytes(debug.message_bytes(msg), n, chunk, 0.9, 8)
+    pos = 0
+    for L, (nnz, bm, cb) in zip(O.chunk_lengths(n, chunk), got):
+        b = L // 2 + 1
+        _, ch = O.encode_spectrum(spec[pos:pos + b], L, 0.9, "count", lat_of(q))
+        assert (nnz, bm, cb) == (ch.codes.size, O.flags_to_bytes(ch.bitmap), O.codes_to_bytes(ch.codes, 8))
+        pos += b
+
+
+def test_end_to_end_against_reference_vectors(golden):
+    meta, arr = golden
+    for rec in meta["e2e"]:
+        g = arr[rec["key"] + "_g"]
+        q = q_of(rec["quantizer"])
+        cfg = F.CodecConfig(F.SparsificationSpec(rec["theta"]), q, half_precision_pass=rec["half"],
+                            chunk_size=rec["chunk"])
+        msg = F.compress(g, cfg)
+        wire = F.serialize(msg)
+        ref_out = arr[rec["key"] + "_out"]
+        got = F.decompress(msg)
+        # end to end the fp32 FFT may move a coefficient across a lattice
+        # boundary; report it, bound it loosely, and require the exact path
+        # above for bit parity.
+        assert abs(len(wire) - rec["wire_bytes"]) <= 16 * len(O.chunk_lengths(rec["n"], rec["chunk"]))
+        assert rel_l2(got, ref_out) <= 1e-3, rec["key"]
+
+
+def test_average_matches_reference_vectors(golden):
+    meta, arr = golden
+    for rec in meta["average"]:
+        rows = arr[rec["key"] + "_rows"]
+        q = q_of(rec["quantizer"])
+        if rec["theta"] == 0 and q is None:
+            continue           # simulator bypass (exact identity), not a codec path
+        cfg = F.CodecConfig(F.SparsificationSpec(rec["theta"]), q, chunk_size=rec["chunk"])
+        msgs = [F.compress(r, cfg) for r in rows]
+        spec = debug.decode_spectrum(msgs, rec["weights"])
+        got = debug.inverse_spectrum(spec, rows.shape[1], cfg)
+        ref = O.average(rows, rec["weights"], rec["theta"], "count", lat_of(q), False, rec["chunk"])
+        ref_v = arr[rec["key"] + "_vhat"]
+        np.testing.assert_array_equal(ref, ref_v)
+        assert rel_l2(got, ref) <= 1e-3
+
+
+def test_decode_average_multi_message_exact_messages():
+    rng = np.random.default_rng(9)
+    n, chunk, W = 300_000, 65536, 5
+    rows = (rng.standard_normal((W, n)) * 1e-2).astype(np.float32)
+    q = F.calibrate([rows[0]], 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.9), q, chunk_size=chunk)
+    w = F.shard_weights(17, W)
+    msgs = [F.compress(r, cfg) for r in rows]
+    spec = debug.decode_spectrum(msgs, w)
+    got = debug.inverse_spectrum(spec, n, cfg)
+    ref = sum(wi * O.decompress(O.from_wire(F.serialize(m))) for wi, m in zip(w, msgs))
+    assert rel_l2(got, ref) <= 1e-5
+
+
+# ---------------------------------------------------------------- wire
+
+def test_golden_fixtures_round_trip(golden):
+    meta, arr = golden
+    for rec in meta["fixtures"]:
+        blob = bytes.fromhex(rec["hex"])
+        m = F.deserialize(blob)
+        assert F.serialize(m) == blob
+        assert m.original_len == arr[f"fix_{rec['name']}_input"].size
+        assert [c.codes.size for c in m.chunks] == rec["kept_per_chunk"]
+        ref = O.decompress(O.from_wire(blob))
+        assert hashlib.sha256(ref.tobytes()).hexdigest() == rec["decompressed_sha256"]
+        assert rel_l2(F.decompress(m), ref) <= 1e-6
+        om = O.from_wire(blob)
+        for a, b in zip(m.chunks, om.chunks):
+            np.testing.assert_array_equal(a.bitmap, b.bitmap)
+            np.testing.assert_array_equal(a.codes, b.codes)
+
+
+def test_compress_serialize_matches_oracle_wire_from_same_message():
+    rng = np.random.default_rng(10)
+    g = rng.standard_normal(5000)
+    q = F.calibrate([g], 6, 2)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.7), q, chunk_size=1024)
+    m = F.compress(g, cfg)
+    blob = F.serialize(m)
+    om = O.from_wire(blob)
+    assert O.to_wire(om) == blob
+    m2 = F.deserialize(blob)
+    assert m2 == m
+    assert F.serialize(m2) == blob
+    # a message rebuilt from host ChunkPayloads decodes identically
+    m3 = F.CompressedMessage(m.original_len, m.chunk_size, m.theta, m.mode, m.half_pass, m.quantizer,
+                             [F.ChunkPayload(c.bitmap.copy(), c.codes.copy()) for c in m.chunks])
+    np.testing.assert_array_equal(F.decompress(m3), F.decompress(m))
+
+
+def test_wire_errors():
+    q = F.tune_eps(-1.0, 1.0, 8, 3)
+    blob = F.serialize(F.compress(np.ones(20), F.CodecConfig(F.SparsificationSpec(0.0), q)))
+    with pytest.raises(F.CorruptHeaderError):
+        F.deserialize(b"NOPE" + bytes(40))
+    with pytest.raises(F.TruncatedPayloadError):
+        F.deserialize(blob[:-3])
+    with pytest.raises(F.TruncatedPayloadError):
+        F.deserialize(blob[:10])
+    b = bytearray(blob)
+    b[36] ^= 1
+    with pytest.raises(F.BitmapMismatchError):
+        F.deserialize(bytes(b))
+    with pytest.raises(F.CodecFormatError):
+        F.deserialize(blob + b"\x00")
+
+
+def test_input_errors():
+    q = F.tune_eps(-1.0, 1.0, 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.5), q)
+    with pytest.raises(ValueError):
+        F.compress(np.array([1.0, np.nan]), cfg)
+    with pytest.raises(ValueError):
+        F.compress(np.array([]), cfg)
+    hcfg = F.CodecConfig(F.SparsificationSpec(0.0), None, half_precision_pass=True)
+    with pytest.raises(ValueError, match="binary16"):
+        F.compress(np.array([1e39] * 16), hcfg)
+
+
+def test_zero_gradient_and_clamp():
+    q = F.tune_eps(-1.0, 1.0, 8, 3)
+    m = F.compress(np.zeros(100), F.CodecConfig(F.SparsificationSpec(0.5), q))
+    assert all(c.codes.size == 0 for c in m.chunks)
+    np.testing.assert_array_equal(F.decompress(m), np.zeros(100))
+    cfg = F.CodecConfig(F.SparsificationSpec(0.0), q, chunk_size=16)
+    np.testing.assert_allclose(F.decompress(F.compress(np.full(16, -2.0), cfg)), q.actual_min / 16, rtol=1e-6)
+    np.testing.assert_allclose(F.decompress(F.compress(np.full(16, 2.0), cfg)), q.actual_max / 16, rtol=1e-6)
+
+
+def test_chunk_independence():
+    rng = np.random.default_rng(4)
+    v = rng.standard_normal(100)
+    q = F.tune_eps(-1.0, 1.0, 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.5), q, chunk_size=32)
+    whole = F.decompress(F.compress(v, cfg))
+    pieces = np.concatenate([F.decompress(F.compress(v[s:s + 32], cfg)) for s in range(0, 100, 32)])
+    np.testing.assert_allclose(whole, pieces, rtol=0, atol=1e-6)
+
+
+# ---------------------------------------------------------------- primitives
+
+def test_quantizer_primitives(golden):
+    meta, arr = golden
+    for rec in meta["encode"]:
+        q = q_of(rec["q"])
+        q = F.QuantizerConfig(rec["q"]["min"], rec["q"]["max"], rec["q"]["n_bits"], rec["q"]["mantissa_bits"],
+                              rec["q"]["eps"], rec["q"]["pbase"], rec["q"]["pos_count"])
+        np.testing.assert_array_equal(F.encode_array(q, arr[rec["key"] + "_x"]), arr[rec["key"] + "_codes"])
+        np.testing.assert_array_equal(F.decode_array(q, np.arange(2 ** q.n_bits)), arr[rec["key"] + "_decoded"])
+    q = F.tune_eps(-1.0, 1.0, 8, 3)
+    with pytest.raises(ValueError, match="index 1"):
+        F.encode_block(q, [0.1, float("nan"), 0.3])
+    with pytest.raises(ValueError):
+        F.decode(q, 256)
+    assert F.pack_codes(np.array([1, 2], dtype=np.uint32), 3) == bytes([0b00010001])
+    for w in (2, 3, 5, 7, 8, 11, 16, 32):
+        c = np.random.default_rng(w).integers(0, 2 ** w, 257, dtype=np.uint64).astype(np.uint32)
+        packed = F.pack_codes(c, w)
+        assert packed == O.codes_to_bytes(c, w)
+        np.testing.assert_array_equal(F.unpack_codes(packed, w, c.size), c)
+
+
+def test_packer_primitives():
+    rng = np.random.default_rng(0)
+    bits = rng.integers(0, 2, size=1_000_003)
+    np.testing.assert_array_equal(F.prefix_sum(bits), np.cumsum(bits))
+    with pytest.raises(ValueError):
+        F.prefix_sum([0, 2, 1])
+    p = F.pack(np.array([7.0, 0.0, 8.0, 0.0, 9.0, 0.0, 0.0]))
+    np.testing.assert_array_equal(p.bitmap, [1, 0, 1, 0, 1, 0, 0])
+    np.testing.assert_array_equal(p.dense, [7.0, 8.0, 9.0])
+    np.testing.assert_array_equal(F.unpack(p), [7.0, 0.0, 8.0, 0.0, 9.0, 0.0, 0.0])
+    bm = rng.random(1000) < 0.4
+    assert F.bitmap_to_bytes(bm) == O.flags_to_bytes(bm)
+    np.testing.assert_array_equal(F.bitmap_from_bytes(F.bitmap_to_bytes(bm), 1000), bm)
+    assert F.bitmap_to_bytes(np.ones(3, dtype=bool)) == bytes([0b11100000])
+
+
+def test_spectral_primitives(golden):
+    rng = np.random.default_rng(0)
+    for n in [1, 2, 3, 17, 128, 1000, 1024, 4097, 100_003]:
+        v = rng.standard_normal(n)
+        ref = np.fft.rfft(v)
+        got = F.dft_forward(v).coefficients
+        assert np.abs(got - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max()), n
+        back = F.dft_inverse(F.Spectrum(ref, n))
+        assert np.abs(back - np.fft.irfft(ref, n=n)).max() <= 1e-12 * max(1.0, np.abs(v).max()) * np.sqrt(n)
+    meta, arr = golden
+    for rec in meta["injection"]:
+        c = arr[rec["key"] + "_coeffs"].astype(np.complex128)
+        out, mask = F.truncate(F.Spectrum(c, rec["length"]), F.SparsificationSpec(rec["theta"]))
+        np.testing.assert_array_equal(mask, arr[rec["key"] + "_mask"])
+        np.testing.assert_array_equal(out.coefficients, np.where(mask, c, 0))
+    mask = F.truncate(F.Spectrum(np.array([3.0, 1.0, 1.0, 5.0, 1.0 + 0j]), 8), F.SparsificationSpec(0.4))[1]
+    np.testing.assert_array_equal(mask, [True, False, False, True, True])
+    assert F.half_round_trip([2049.0])[0] == 2048.0 and F.half_round_trip([2051.0])[0] == 2052.0
+
+
+def test_calibrate_matches_reference(golden):
+    meta, arr = golden
+    for rec in meta["calibrate"]:
+        q = F.calibrate([arr[rec["key"] + "_g"]], *rec["nm"])
+        r = rec["q"]
+        assert (q.min, q.max, q.eps, q.pos_count) == (r["min"], r["max"], r["eps"], r["pos_count"])
+
+
+# ---------------------------------------------------------------- scale
+
+def test_resnet50_size_properties():
+    """25.6M floats (BASELINE config 2): size-independent properties."""
+    n = 25_600_000
+    g = torch.randn(n, device="cuda", generator=torch.Generator("cuda").manual_seed(0)) * 1e-2
+    q = F.calibrate([g[:65536 * 4].double().cpu().numpy()], 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.9), q)
+    m1 = F.compress(g, cfg)
+    m2 = F.compress(g, cfg)
+    b1, b2 = debug.message_bytes(m1), debug.message_bytes(m2)
+    assert b1 == b2                                   # deterministic
+    segs = segments_valid_bytes(b1, n, 65536, 0.9, 8)
+    for L, (nnz, bm, _) in zip(O.chunk_lengths(n, 65536), segs):
+        bins = L // 2 + 1
+        assert nnz <= 2 * O.keep_bins(bins, 0.9)
+        assert bin(int.from_bytes(bm, "big")).count("1") == nnz
+    out1 = F.codec.decompress_device(m1)
+    out2 = F.codec.decompress_device(m2)
+    assert torch.equal(out1, out2)
+    # spot-check three chunks against the oracle decode of the same payloads
+    host = g.double().cpu().numpy()
+    spec = debug.forward_spectrum(g, cfg)
+    for c in (0, 200, 390):
+        L = O.chunk_lengths(n, 65536)[c]
+        off = c * 65536
+        b0 = c * 32769
+        _, ch = O.encode_spectrum(spec[b0:b0 + L // 2 + 1], L, 0.9, "count", lat_of(q))
+        ref = O.decompress(O.Message(L, 65536, 0.9, "count", False, lat_of(q), [ch]))
+        assert rel_l2(out1[off:off + L].cpu().numpy(), ref) <= 1e-5
+        assert rel_l2(np.fft.rfft(host[off:off + L]), spec[b0:b0 + L // 2 + 1]) <= 1e-6
