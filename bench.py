@@ -1,0 +1,352 @@
+"""Benchmark: gradient GB/s through compress + allgather + decompress/average
+(BASELINE.json `metric`) on synthetic ResNet-50-sized gradients.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = every rank compresses its own n-float gradient (weak scaling),
+allgathers the fixed-capacity messages over NCCL, and decodes the weighted
+average of all W messages (frequency-domain accumulate + one iFFT per chunk).
+
+value : whole-job GB/s = W * 4n bytes / (max-over-ranks device time of one
+        step), inputs resident in HBM, L2 flushed (256 MB write) between
+        timed steps, CUDA events on the launching stream.
+e2e   : same metric through the public API with pinned host buffers: H2D of
+        the gradient, the step, D2H of the averaged gradient, all timed.
+--impl reference: the reference's CPU implementation of the path (the oracle
+        port, chunk-parallel over all host cores), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # BASELINE.json configs[1]: ResNet-50-sized gradient, keep 0.1 (reference theta=0.9 drop), 8-bit range float
+    "resnet50": dict(n=25_600_000, theta=0.9, n_bits=8, mbits=3, chunk=65536),
+    "cpu1m": dict(n=1_000_000, theta=0.9, n_bits=8, mbits=3, chunk=65536),
+    "alexnet": dict(n=61_000_000, theta=0.9, n_bits=8, mbits=3, chunk=65536),
+    "vgg16": dict(n=138_000_000, theta=0.9, n_bits=8, mbits=3, chunk=65536),
+}
+METRIC = "gradient GB/s through compress+sync+decompress; sync ms/step at 1/2/4/8 B200"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- reference arm
+
+def _ref_chunk_job(args):
+    g_bytes, theta, lat, chunk = args
+    import oracle as O
+    g = np.frombuffer(g_bytes, dtype=np.float32).astype(np.float64)
+    msg = O.compress(g, theta, "count", lat, False, chunk)
+    wire = O.to_wire(msg)
+    return O.decompress(O.from_wire(wire))
+
+
+def cpu_reference(wl: dict, seconds_budget: float, cores: int | None = None, sample_chunks: int | None = None):
+    """The reference CPU path (oracle port of compress -> serialize ->
+    deserialize -> decompress), chunk-parallel over `cores` processes on a
+    bounded sample of the workload.  Returns (GB/s, cores, sample desc)."""
+    import multiprocessing as mp
+
+    import oracle as O
+    cores = cores or len(os.sched_getaffinity(0))
+    chunk = wl["chunk"]
+    rng = np.random.default_rng(0)
+    probe = (rng.standard_normal(chunk) * 1e-2).astype(np.float32)
+    lat = O.calibrate([probe], wl["n_bits"], wl["mbits"])
+    t0 = time.perf_counter()
+    _ref_chunk_job((probe.tobytes(), wl["theta"], lat, chunk))
+    per_chunk = time.perf_counter() - t0
+    if sample_chunks is None:
+        sample_chunks = int(max(cores, min(wl["n"] // chunk, seconds_budget * cores / max(per_chunk, 1e-3))))
+    g = (rng.standard_normal(sample_chunks * chunk) * 1e-2).astype(np.float32)
+    jobs = [(g[i * chunk:(i + 1) * chunk].tobytes(), wl["theta"], lat, chunk) for i in range(sample_chunks)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        t0 = time.perf_counter()
+        pool.map(_ref_chunk_job, jobs, chunksize=max(1, sample_chunks // (4 * cores)))
+        dt = time.perf_counter() - t0
+    gbs = 4.0 * sample_chunks * chunk / dt / 1e9
+    return gbs, cores, f"{sample_chunks} chunks x {chunk} floats ({sample_chunks * chunk} floats), {dt:.2f}s"
+
+
+def run_reference(args, wl, rank, world):
+    if rank != 0:
+        return
+    steps = []
+    cores = len(os.sched_getaffinity(0))
+    for i in range(args.warmup + args.steps):
+        gbs, cores, sample = cpu_reference(wl, seconds_budget=max(2.0, 20.0 / max(1, args.steps)), cores=cores)
+        if i >= args.warmup:
+            steps.append(gbs)
+    v = statistics.median(steps)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 4.0 * wl["n"] / (v * 1e9) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic gaussian sigma=1e-2",
+            "config": workload_config(args, wl, world),
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, wl, world):
+    return {"workload": f"{args.workload}: n={wl['n']} floats, keep={1 - wl['theta']:.2f} "
+                        f"(reference theta_drop={wl['theta']}), {wl['n_bits']}-bit range float m={wl['mbits']}, "
+                        f"chunk={wl['chunk']}, W={world} ranks",
+            "n": wl["n"], "theta_drop": wl["theta"], "n_bits": wl["n_bits"], "mantissa_bits": wl["mbits"],
+            "chunk_size": wl["chunk"], "world": world, "parallelism": f"dp{world}",
+            "l2": "flushed between timed steps (256 MB write)"}
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_ours(args, wl, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1811_08596_b200 as F
+    from paper_1811_08596_b200.comm import GradientAverager, NcclComm
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n = wl["n"]
+    # quantizer calibrated once on rank 0's gradient (every rank regenerates it)
+    g0 = torch.randn(n, device=dev, generator=torch.Generator(dev).manual_seed(1000)) * 1e-2
+    q = F.calibrate([g0], wl["n_bits"], wl["mbits"])
+    del g0
+    cfg = F.CodecConfig(F.SparsificationSpec(wl["theta"]), q, chunk_size=wl["chunk"])
+    grad = torch.randn(n, device=dev, generator=torch.Generator(dev).manual_seed(1000 + rank)) * 1e-2
+    comm = NcclComm() if world > 1 else None
+    weights = np.full(world, 1.0 / world)
+    avg = GradientAverager(n, cfg, weights, comm)
+    M = avg.plan.message_bytes
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timing, per-stage events
+    from paper_1811_08596_b200 import _lib, _device as D
+    import ctypes as C
+
+    def one_step(ev=None):
+        if ev is None:
+            avg.step(grad)
+            return
+        ev[0].record()
+        _lib.check(_lib.lib.fgc_compress(avg.plan.handle, grad.data_ptr(), _lib.DTYPE_F32, avg.message.data_ptr(),
+                                         avg.flags.data_ptr(), D.stream()))
+        ev[1].record()
+        if world > 1:
+            comm.allgather(avg.message, avg.gathered)
+        ev[2].record()
+        _lib.check(_lib.lib.fgc_decode_average(avg.plan.handle, avg.gathered.data_ptr(), world, M,
+                                               avg.weights.ctypes.data, avg.out.data_ptr(), D.stream()))
+        ev[3].record()
+
+    for _ in range(max(3, args.warmup)):
+        flush.fill_(1.0)
+        one_step()
+    barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    launches0 = F.kernel_launches()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            one_step(evs[i])
+        barrier()
+    launches = F.kernel_launches() - launches0
+    avg.check()
+    st = np.array([[evs[i][0].elapsed_time(evs[i][1]), evs[i][1].elapsed_time(evs[i][2]),
+                    evs[i][2].elapsed_time(evs[i][3])] for i in range(args.steps)])
+    step_ms = st.sum(axis=1)
+    local = np.array([step_ms.mean(), st[:, 0].mean(), st[:, 1].mean(), st[:, 2].mean()])
+    if world > 1:
+        t = torch.tensor(local, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        local = t.cpu().numpy()
+    ms, c_ms, s_ms, d_ms = [float(x) for x in local]
+
+    # ---- uncompressed baseline collective: fp32 allreduce of the gradient
+    allreduce_ms = None
+    if world > 1:
+        buf = grad.clone()
+        for _ in range(3):
+            comm.allreduce_sum_(buf)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            comm.allreduce_sum_(buf)
+        e1.record()
+        barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce_ms = float(t.item())
+
+    # ---- end to end through the public API with pinned host buffers
+    host_in = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    host_in.copy_(grad.cpu())
+    host_out = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    dgrad = torch.empty(n, dtype=torch.float32, device=dev)
+
+    def e2e_step():
+        dgrad.copy_(host_in, non_blocking=True)
+        out = avg.step(dgrad)
+        host_out.copy_(out, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank != 0:
+        return
+    hbm, peak_kind = peaks()
+    job_bytes = 4.0 * n * world
+    value = job_bytes / (ms * 1e-3) / 1e9
+    # roofline of the dominant kernel (algorithmic bytes per launch / its time)
+    comp_bytes = 4.0 * n + M
+    dec_bytes = float(world) * M + 4.0 * n
+    dom = ("compress", comp_bytes, c_ms) if c_ms >= d_ms else ("decode_average", dec_bytes, d_ms)
+    achieved = dom[1] / (dom[2] * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic gaussian sigma=1e-2 (torch.randn, seed 1000+rank)",
+        "config": workload_config(args, wl, world),
+        "sync_ms": ms, "stages_ms": {"compress": c_ms, "allgather": s_ms, "decode_average": d_ms},
+        "allreduce_fp32_ms": allreduce_ms,
+        "message_bytes": M, "compression_ratio": 4.0 * n / M,
+        "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "algorithmic_bytes": dom[1],
+                     "step_frac": ((comp_bytes + dec_bytes) / ((c_ms + d_ms) * 1e-3) / 1e9) / hbm},
+        "e2e": {"value": job_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        gbs, cores, sample = cpu_reference(wl, seconds_budget=15.0)
+        line["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="resnet50", choices=sorted(WORKLOADS))
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = dict(WORKLOADS[args.workload])
+    if args.n:
+        wl["n"] = args.n
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, wl, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, wl, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -356,6 +356,11 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
     seg[0] = rank_base;
     seg[1] = 0; seg[2] = 0; seg[3] = 0;
   }
+  // deterministic padding: bitmap pad words and the unused code capacity
+  const uint32_t used = (uint32_t)(((uint64_t)rank_base * N + 31) / 32);
+  for (uint32_t w = bm_words + tid; w < (ci.code_off - kSegHeader) / 4; w += kSelThreads) bitmap[w] = 0;
+  const uint32_t cap_padded = (ci.code_cap + 3u) & ~3u;
+  for (uint32_t w = used + tid; w < cap_padded; w += kSelThreads) codes[w] = 0;
   // zero the bitmap tail words beyond the last tile (none: tiles cover bins)
   if (overflow) atomicOr(flags, FGC_FLAG_CAPACITY);
 }
