@@ -112,9 +112,11 @@ enum SelMode : int { kKeepAll = 0, kDropAll = 1, kList = 2, kExact = 3 };
 template <typename CT>
 __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* chunks, uint32_t first, Coeffs<CT> coeffs,
                                                              int exact_only, QuantParams q, uint8_t* message,
-                                                             uint8_t* kept_mask, uint32_t* flags) {
+                                                             uint8_t* kept_mask, uint32_t* flags,
+                                                             const uint32_t* only_if) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SelectShared& sh = *reinterpret_cast<SelectShared*>(smem_raw);
+  if (only_if && only_if[first + blockIdx.x] == 0u) return;
   const ChunkInfo ci = chunks[first + blockIdx.x];
   const uint32_t B = ci.bins;
   const uint32_t kdrop = ci.drop;
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(kDecThreads) k_decode_accumulate(const ChunkIn
 
 fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_t count, const void* spectrum,
                               int coeff_f64, const QuantParams& q, uint8_t* message, uint8_t* kept_mask,
-                              uint32_t* flags, cudaStream_t s) {
+                              uint32_t* flags, cudaStream_t s, const uint32_t* only_if) {
   if (!count) return FGC_OK;
   static bool attr = false;
   const size_t smem = sizeof(SelectShared);
@@ -436,10 +438,12 @@ fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_
   }
   if (coeff_f64) {
     Coeffs<double2> c{static_cast<const double2*>(spectrum)};
-    k_select_pack<double2><<<count, kSelThreads, smem, s>>>(d_chunks, first, c, 1, q, message, kept_mask, flags);
+    k_select_pack<double2><<<count, kSelThreads, smem, s>>>(d_chunks, first, c, 1, q, message, kept_mask, flags,
+                                                            only_if);
   } else {
     Coeffs<float2> c{static_cast<const float2*>(spectrum)};
-    k_select_pack<float2><<<count, kSelThreads, smem, s>>>(d_chunks, first, c, 0, q, message, kept_mask, flags);
+    k_select_pack<float2><<<count, kSelThreads, smem, s>>>(d_chunks, first, c, 0, q, message, kept_mask, flags,
+                                                           only_if);
   }
   FGC_LAUNCHED(1);
   return FGC_OK;

@@ -121,9 +121,10 @@ fgc_status real_inverse(RealClassT<R>& rc, const ChunkInfo* d_chunks, const type
 
 // Select (count mode) + quantize + pack from a chunk-major spectrum.
 // Chunks [first, first+count).  coeff_f64: spectrum is double2.
+// only_if (may be null): skip chunk c unless only_if[c] != 0.
 fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_t count, const void* spectrum,
                               int coeff_f64, const QuantParams& q, uint8_t* message, uint8_t* kept_mask,
-                              uint32_t* flags, cudaStream_t s);
+                              uint32_t* flags, cudaStream_t s, const uint32_t* only_if = nullptr);
 
 // Decode + weighted accumulate of W messages into a chunk-major spectrum.
 struct Weights {
@@ -154,9 +155,11 @@ struct FusedTables;
 bool fused_available();
 fgc_status fused_tables_init(FusedTables** t, cudaStream_t s);
 void fused_tables_free(FusedTables* t);
+// fb: per-chunk fallback flags (1 = chunk left to the generic select kernel,
+// whose spectrum was written to fb_spec).
 fgc_status launch_fused_compress(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                  const void* grad, int dtype, int half_pass, const QuantParams& q, uint8_t* message,
-                                 uint32_t* flags, cudaStream_t s);
+                                 uint32_t* flags, uint32_t* fb, float2* fb_spec, cudaStream_t s);
 fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
                                const QuantParams& q, float* out, cudaStream_t s);

@@ -1,33 +1,805 @@
-// Fused sm_100a kernels for 65536-sample chunks: placeholder until the
-// cluster kernels land (the generic path handles every length meanwhile).
+// Fused sm_100a kernels for 65536-sample chunks (the codec's default and the
+// benchmark's chunk size, codec.py:73).  One chunk per thread-block cluster
+// of two CTAs; everything between the HBM read of the gradient and the HBM
+// write of the message happens on chip.
+//
+// compress (k_fused_compress, cluster 2x1x1, 512 threads per CTA)
+//   z[n] = x[2n] + i x[2n+1], N = 32768 complex points.  A decimation-in-
+//   frequency split gives each CTA an independent 16384-point FFT:
+//     CTA 0: a[n] = z[n] + z[n+M]             -> Z[2m]   = FFT_M(a)[m]
+//     CTA 1: b[n] = (z[n] - z[n+M]) W_N^n     -> Z[2m+1] = FFT_M(b)[m]
+//   (each CTA reads the whole chunk; the second read hits L2).  The real-FFT
+//   post-processing pairs Z[k] with Z[N-k]; both stay inside one CTA and, by
+//   choosing pass-3 columns (k, 1024-k) / (k, 1023-k), inside one thread.
+//   So the 32769 bins X[k] end up in registers: even bins in CTA 0, odd bins
+//   in CTA 1.  Count-mode selection (spectral.py:124-156) is a cluster-wide
+//   radix select on a float32 proxy of |X|^2 (histograms merged through
+//   DSMEM), with numpy's exact float64 cabs key and the stable index
+//   tie-break applied to the few bins whose proxy is too close to call.
+//   Codes (quantizer.py:217-236) are gathered bin-ordered into CTA 0's shared
+//   memory (CTA 1 stores its non-zero pairs remotely) and CTA 0 emits the
+//   MSB-first bitmap and the LSB-first packed code stream (packer.py,
+//   quantizer.pack_codes) straight into the device message segment.
+//   Degenerate chunks (all proxies tiny, or > kCand undecided bins) are
+//   handed to the generic select kernel via a per-chunk flag.
+//
+// decode (k_fused_decode, 2 CTAs per chunk, 512 threads)
+//   CTA r builds Y_r (16384 complex, shared memory) directly from the W
+//   messages: every non-zero slot of bin b adds its weighted value into the
+//   two entries its bin feeds (Z[b] and Z[N-b], folded mod M), processed in
+//   four bin quarters so no two threads ever touch the same entry (fixed
+//   worker order -> deterministic, identical on every rank).  One inverse
+//   16384-point FFT per CTA then yields the even (r=0) or odd (r=1) complex
+//   samples of the chunk: x[4p+2r], x[4p+2r+1].
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <math.h>
+
+#include "fgc_device.cuh"
 #include "fgc_internal.h"
+#include "fused_fft.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace fgc {
 
-struct FusedTables {};
+struct FusedTables {
+  float2* thi = nullptr;   // W_65536^(256 h), h < 256
+  float2* tlo = nullptr;   // W_65536^l, l < 256
+};
 
-bool fused_available() { return false; }
-fgc_status fused_tables_init(FusedTables** t, cudaStream_t) {
-  *t = nullptr;
-  set_error("fused kernels unavailable");
-  return FGC_ERR_UNSUPPORTED;
+namespace {
+
+using namespace ff;
+
+constexpr int kCand = 1024;
+constexpr uint32_t kBins = kN + 1;           // 32769
+constexpr uint32_t kBmWords = (2 * kBins + 31) / 32;   // 2049
+
+__global__ void k_init_tables(float2* thi, float2* tlo) {
+  const int i = threadIdx.x;
+  double s, c;
+  sincospi(-2.0 * (double)(256 * i) / 65536.0, &s, &c);
+  thi[i] = make_float2((float)c, (float)s);
+  sincospi(-2.0 * (double)i / 65536.0, &s, &c);
+  tlo[i] = make_float2((float)c, (float)s);
 }
-void fused_tables_free(FusedTables*) {}
-fgc_status launch_fused_compress(const FusedTables*, const ChunkInfo*, uint32_t, uint32_t, const void*, int, int,
-                                 const QuantParams&, uint8_t*, uint32_t*, cudaStream_t) {
-  return FGC_ERR_UNSUPPORTED;
+
+// ------------------------------------------------------------------ loads
+
+template <class T> struct In;
+template <> struct In<float> {
+  __device__ static float2 get(const float* g, uint64_t e, int half, uint32_t& bad) {
+    float2 v = *reinterpret_cast<const float2*>(g + e);
+    if (!isfinite(v.x) || !isfinite(v.y)) { bad |= FGC_FLAG_NONFINITE; v = make_float2(0.f, 0.f); }
+    if (half) {
+      v.x = __half2float(__float2half_rn(v.x));
+      v.y = __half2float(__float2half_rn(v.y));
+      if (isinf(v.x) || isinf(v.y)) bad |= FGC_FLAG_HALF_OVERFLOW;
+    }
+    return v;
+  }
+};
+template <> struct In<double> {
+  __device__ static float2 get(const double* g, uint64_t e, int half, uint32_t& bad) {
+    const double2 d = *reinterpret_cast<const double2*>(g + e);
+    if (!isfinite(d.x) || !isfinite(d.y)) { bad |= FGC_FLAG_NONFINITE; return make_float2(0.f, 0.f); }
+    float2 v;
+    if (half) {
+      v = make_float2(__half2float(__double2half(d.x)), __half2float(__double2half(d.y)));
+      if (isinf(v.x) || isinf(v.y)) bad |= FGC_FLAG_HALF_OVERFLOW;
+    } else {
+      v = make_float2((float)d.x, (float)d.y);
+      if (isinf(v.x) || isinf(v.y)) bad |= FGC_FLAG_F32_RANGE;
+    }
+    return v;
+  }
+};
+
+// ------------------------------------------------------------------ compress
+
+struct CompressArgs {
+  const ChunkInfo* chunks;
+  uint32_t first;
+  const void* grad;
+  int half;
+  QuantParams q;
+  uint8_t* message;
+  uint32_t* flags;
+  const float2* thi;
+  const float2* tlo;
+  uint32_t* fb;          // per-chunk fallback flag (indexed by chunk id)
+  float2* fb_spec;       // chunk-major spectrum scratch for fallback chunks
+  float2* dbg_spec;      // debug hook: write the spectrum and stop
+};
+
+struct __align__(16) CompressShared {
+  float2 buf[kPadded + 64];          // FFT transposes, then the bin-ordered code array
+  float2 thi[256], tlo[256];
+  uint32_t hist[2048];
+  uint32_t scan[40];
+  unsigned long long ckey[kCand];    // CTA 0: undecided bins (exact key, bin)
+  uint32_t cidx[kCand];
+  uint32_t ccount;                   // CTA 0: number of undecided bins
+  uint32_t below;                    // per CTA: bins certainly dropped
+  uint32_t anynz;                    // per CTA: any non-zero coefficient
+  uint32_t fbin, fbelow;             // find_bucket result
+  int mode;                          // CTA 0's decision, read by CTA 1
+  uint32_t need;
+};
+
+enum : int { kModeKeepAll = 0, kModeDropAll = 1, kModeList = 2, kModeFallback = 3 };
+
+// Bucket holding rank r in the cluster-merged histogram (own + peer).
+__device__ void merged_bucket(CompressShared& sh, const uint32_t* peer_hist, uint32_t r, uint32_t& bucket,
+                              uint32_t& below) {
+  const uint32_t t = threadIdx.x;
+  uint32_t h[4], local = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    h[q] = sh.hist[4 * t + q] + peer_hist[4 * t + q];
+    local += h[q];
+  }
+  uint32_t total;
+  const uint32_t before = block_exclusive_scan<kThreads>(local, sh.scan, total);
+  if (r >= before && r < before + local) {
+    uint32_t acc = before;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (r >= acc && r < acc + h[q]) {
+        sh.fbin = 4 * t + q;
+        sh.fbelow = acc;
+      }
+      acc += h[q];
+    }
+  }
+  __syncthreads();
+  bucket = sh.fbin;
+  below = sh.fbelow;
 }
-fgc_status launch_fused_decode(const FusedTables*, const ChunkInfo*, uint32_t, uint32_t, const uint8_t*, int,
-                               uint64_t, const Weights&, const QuantParams&, float*, cudaStream_t) {
-  return FGC_ERR_UNSUPPORTED;
+
+// Histogram add with warp aggregation of equal buckets.
+__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bucket, bool active) {
+  const uint32_t am = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  const uint32_t peers = __match_any_sync(am, bucket);
+  if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&hist[bucket], (uint32_t)__popc(peers));
 }
-fgc_status launch_fused_spectrum(const FusedTables*, const ChunkInfo*, uint32_t, uint32_t, const void*, int, int,
-                                 float2*, uint32_t*, cudaStream_t) {
-  return FGC_ERR_UNSUPPORTED;
+
+template <class T, bool DEBUG>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused_compress(CompressArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CompressShared& sh = *reinterpret_cast<CompressShared*>(smem_raw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const uint32_t r = cluster.block_rank();
+  const uint32_t tid = threadIdx.x;
+  const uint32_t chunk = a.first + blockIdx.x / 2;
+  const ChunkInfo ci = a.chunks[chunk];
+  CompressShared& sh0 = *cluster.map_shared_rank(&sh, 0);
+  CompressShared& shp = *cluster.map_shared_rank(&sh, r ^ 1);
+
+  if (tid < 256) {
+    sh.thi[tid] = a.thi[tid];
+    sh.tlo[tid] = a.tlo[tid];
+  }
+  for (uint32_t b = tid; b < 2048; b += kThreads) sh.hist[b] = 0;
+  if (tid == 0) { sh.ccount = 0; sh.below = 0; sh.anynz = 0; }
+  uint32_t* codes_g = reinterpret_cast<uint32_t*>(a.message + ci.seg_off + ci.code_off);
+  const uint32_t cap_padded = (ci.code_cap + 3u) & ~3u;
+  if (!DEBUG && r == 0)
+    for (uint32_t w = tid; w < cap_padded; w += kThreads) codes_g[w] = 0;   // red.or targets
+  __syncthreads();
+
+  // ---- 1. load + decimation-in-frequency split (pass-1 input layout)
+  float2 v[32];
+  {
+    const T* g = static_cast<const T*>(a.grad) + ci.in_off;
+    uint32_t bad = 0;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t n = tid + 512u * j;
+      const float2 z0 = In<T>::get(g, 2ull * n, a.half, bad);
+      const float2 z1 = In<T>::get(g, 2ull * (n + kM), a.half, bad);
+      if (r == 0) {
+        v[j] = make_float2(z0.x + z1.x, z0.y + z1.y);
+      } else {
+        v[j] = cmul(make_float2(z0.x - z1.x, z0.y - z1.y), tw(sh.thi, sh.tlo, 2u * n));   // W_N^n
+      }
+    }
+    if (bad && r == 0) atomicOr(a.flags, bad);
+  }
+
+  // ---- 2. 16384-point FFT: passes 1, 2 (transposes in smem), pass 3 on two columns
+  fft_pass12<false>(v, sh.buf, sh.thi, sh.tlo);
+  __syncthreads();
+  uint32_t ka, kb;
+  if (r == 0) {
+    ka = tid;
+    kb = tid == 0 ? 512u : 1024u - tid;
+  } else {
+    ka = tid;
+    kb = 1023u - tid;
+  }
+  float2 va[16], vb[16];
+  fft_pass3<false>(ka, sh.buf, va, sh.thi, sh.tlo);
+  fft_pass3<false>(kb, sh.buf, vb, sh.thi, sh.tlo);
+
+  // ---- 3. real-FFT post-processing in registers: X[k] = (P + conj Q)/2 - i W_L^k (P - conj Q)/2
+  auto r2c = [&](float2 P, float2 Q, uint32_t bin) -> float2 {
+    const float2 A = make_float2(P.x + Q.x, P.y - Q.y);
+    const float2 B = make_float2(P.x - Q.x, P.y + Q.y);
+    const float2 t = cmul(tw(sh.thi, sh.tlo, bin), make_float2(B.y, -B.x));
+    return make_float2(0.5f * (A.x + t.x), 0.5f * (A.y + t.y));
+  };
+  float2 xn = make_float2(0.f, 0.f);      // X[N] (CTA 0, thread 0 only)
+  const bool special = (r == 0 && tid == 0);
+  if (!special) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float2 P = va[j], Q = vb[15 - j];
+      const uint32_t ma = ka + 1024u * j, mb = kb + 1024u * (15 - j);
+      va[j] = r2c(P, Q, 2u * ma + r);
+      vb[15 - j] = r2c(Q, P, 2u * mb + r);
+    }
+  } else {
+    // column 0: pairs j <-> 16-j, self pairs j = 0 (X[0], X[N]) and j = 8 (X[M])
+    const float2 a0 = va[0], a8 = va[8];
+    float2 tmp[16];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+      tmp[j] = r2c(va[j], va[16 - j], 2u * 1024u * j);
+      tmp[16 - j] = r2c(va[16 - j], va[j], 2u * 1024u * (16 - j));
+    }
+#pragma unroll
+    for (int j = 1; j < 16; ++j) if (j != 8) va[j] = tmp[j];
+    va[0] = make_float2(a0.x + a0.y, 0.f);
+    xn = make_float2(a0.x - a0.y, 0.f);
+    va[8] = r2c(a8, a8, 2u * 1024u * 8);
+    // column 512: pairs j <-> 15-j
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float2 P = vb[j], Q = vb[15 - j];
+      vb[j] = r2c(P, Q, 2u * (512u + 1024u * j));
+      vb[15 - j] = r2c(Q, P, 2u * (512u + 1024u * (15 - j)));
+    }
+  }
+  // bin of register entry: va[j] -> 2 (ka + 1024 j) + r, vb[j] -> 2 (kb + 1024 j) + r
+#define BIN_A(j) (2u * (ka + 1024u * (j)) + r)
+#define BIN_B(j) (2u * (kb + 1024u * (j)) + r)
+
+  if (DEBUG) {
+    float2* out = a.dbg_spec + ci.bin_off;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      out[BIN_A(j)] = va[j];
+      out[BIN_B(j)] = vb[j];
+    }
+    if (special) out[kN] = xn;
+    return;
+  }
+
+  // ---- 4. count-mode selection, cluster-wide
+  const uint32_t kdrop = ci.drop;
+  int mode = kModeList;
+  if (kdrop == 0) mode = kModeKeepAll;
+  else if (kdrop >= kBins) mode = kModeDropAll;
+  float band_lo = 0.f, band_hi = INFINITY;
+  if (mode == kModeList) {
+    // pass 1: proxy bits [30:20]
+    uint32_t nz = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float pa = proxy_key(va[j].x, va[j].y), pb = proxy_key(vb[j].x, vb[j].y);
+      nz |= __float_as_uint(pa) | __float_as_uint(pb);
+      hist_add(sh.hist, __float_as_uint(pa) >> 20, true);
+      hist_add(sh.hist, __float_as_uint(pb) >> 20, true);
+    }
+    {
+      const float pn = proxy_key(xn.x, xn.y);
+      nz |= __float_as_uint(pn);
+      hist_add(sh.hist, __float_as_uint(pn) >> 20, special);
+    }
+    if (__any_sync(0xffffffffu, nz != 0) && (tid & 31) == 0) atomicOr(&sh.anynz, 1u);
+    cluster.sync();
+    const bool anynz = (sh.anynz | shp.anynz) != 0;
+    uint32_t b1, below1;
+    merged_bucket(sh, shp.hist, kdrop - 1, b1, below1);
+    cluster.sync();                               // peer finished reading my histogram
+    if (!anynz) {
+      mode = kModeDropAll;                        // every coefficient is exactly zero: all codes 0
+    } else {
+      for (uint32_t b = tid; b < 2048; b += kThreads) sh.hist[b] = 0;
+      __syncthreads();
+      // pass 2: proxy bits [19:9] inside bucket b1
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t pa = __float_as_uint(proxy_key(va[j].x, va[j].y));
+        const uint32_t pb = __float_as_uint(proxy_key(vb[j].x, vb[j].y));
+        hist_add(sh.hist, (pa >> 9) & 0x7FFu, (pa >> 20) == b1);
+        hist_add(sh.hist, (pb >> 9) & 0x7FFu, (pb >> 20) == b1);
+      }
+      {
+        const uint32_t pn = __float_as_uint(proxy_key(xn.x, xn.y));
+        hist_add(sh.hist, (pn >> 9) & 0x7FFu, special && (pn >> 20) == b1);
+      }
+      cluster.sync();
+      uint32_t b2, below2;
+      merged_bucket(sh, shp.hist, kdrop - 1 - below1, b2, below2);
+      const uint32_t lo_pat = (b1 << 20) | (b2 << 9);
+      const float lo_f = __uint_as_float(lo_pat);
+      const float hi_f = __uint_as_float(lo_pat + 512u);
+      if (lo_f < 0x1p-100f || hi_f > 0x1p100f) {
+        mode = kModeFallback;
+      } else {
+        band_lo = lo_f * (1.0f - 0x1p-16f);
+        band_hi = hi_f * (1.0f + 0x1p-16f);
+        // collect undecided bins into CTA 0's list; count the certainly dropped
+        uint32_t below_l = 0;
+        auto collect = [&](float2 x, uint32_t bin, bool act) {
+          if (!act) return;
+          const float p = proxy_key(x.x, x.y);
+          if (p < band_lo) {
+            ++below_l;
+          } else if (p < band_hi) {
+            const uint32_t s = atomicAdd(&sh0.ccount, 1u);
+            if (s < (uint32_t)kCand) {
+              sh0.cidx[s] = bin;
+              sh0.ckey[s] = (unsigned long long)__double_as_longlong(cabs_key((double)x.x, (double)x.y));
+            }
+          }
+        };
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          collect(va[j], BIN_A(j), true);
+          collect(vb[j], BIN_B(j), true);
+        }
+        collect(xn, kN, special);
+        const uint32_t bl = block_sum<kThreads>(below_l, sh.scan);
+        if (tid == 0) sh.below = bl;
+      }
+      cluster.sync();
+      // CTA 0 resolves the undecided bins exactly
+      if (r == 0) {
+        __shared__ int dec;
+        if (tid == 0) {
+          int md = mode;
+          const uint32_t m = sh.ccount;
+          const uint32_t below = sh.below + shp.below;
+          if (md == kModeList) {
+            if (m > (uint32_t)kCand || below > kdrop || below + m < kdrop) md = kModeFallback;
+          }
+          sh.need = kdrop - below;
+          dec = md;
+        }
+        __syncthreads();
+        mode = dec;
+        if (mode == kModeList) {
+          const uint32_t m = sh.ccount, need = sh.need;
+          uint32_t M2 = 1;
+          while (M2 < m) M2 <<= 1;
+          for (uint32_t s = m + tid; s < M2; s += kThreads) {
+            sh.ckey[s] = ~0ull;
+            sh.cidx[s] = 0x7FFFFFFFu;
+          }
+          __syncthreads();
+          // sort by (key, bin), mark the `need` smallest dropped, then sort by bin
+          for (int pass = 0; pass < 2; ++pass) {
+            for (uint32_t k = 2; k <= M2; k <<= 1) {
+              for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+                for (uint32_t t = tid; t < M2; t += kThreads) {
+                  const uint32_t u = t ^ jj;
+                  if (u > t) {
+                    const bool asc = (t & k) == 0;
+                    bool gt;
+                    if (pass == 0) {
+                      gt = sh.ckey[t] > sh.ckey[u] ||
+                           (sh.ckey[t] == sh.ckey[u] && (sh.cidx[t] & 0x7FFFFFFFu) > (sh.cidx[u] & 0x7FFFFFFFu));
+                    } else {
+                      gt = (sh.cidx[t] & 0x7FFFFFFFu) > (sh.cidx[u] & 0x7FFFFFFFu);
+                    }
+                    if (gt == asc) {
+                      const unsigned long long tk = sh.ckey[t]; sh.ckey[t] = sh.ckey[u]; sh.ckey[u] = tk;
+                      const uint32_t ti = sh.cidx[t]; sh.cidx[t] = sh.cidx[u]; sh.cidx[u] = ti;
+                    }
+                  }
+                }
+                __syncthreads();
+              }
+            }
+            if (pass == 0) {
+              for (uint32_t s = tid; s < need && s < m; s += kThreads) sh.cidx[s] |= 0x80000000u;
+              __syncthreads();
+            }
+          }
+        }
+        if (tid == 0) sh.mode = mode;
+      }
+      cluster.sync();
+      mode = sh0.mode;
+    }
+  }
+
+  if (mode == kModeFallback) {
+    float2* out = a.fb_spec + ci.bin_off;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      out[BIN_A(j)] = va[j];
+      out[BIN_B(j)] = vb[j];
+    }
+    if (special) out[kN] = xn;
+    if (r == 0 && tid == 0) a.fb[chunk] = 1u;
+    cluster.sync();          // keep both CTAs resident until all DSMEM traffic is done
+    return;
+  }
+  if (r == 0 && tid == 0) a.fb[chunk] = 0u;
+
+  // ---- 5. codes for every register bin
+  const uint32_t mcount = (mode == kModeList) ? sh0.ccount : 0u;
+  auto dropped = [&](float2 x, uint32_t bin) -> bool {
+    if (mode == kModeKeepAll) return false;
+    if (mode == kModeDropAll) return true;
+    const float p = proxy_key(x.x, x.y);
+    if (p < band_lo) return true;
+    if (p >= band_hi) return false;
+    uint32_t lo = 0, hi = mcount;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if ((sh0.cidx[mid] & 0x7FFFFFFFu) < bin) lo = mid + 1; else hi = mid;
+    }
+    return lo < mcount && (sh0.cidx[lo] & 0x7FFFFFFFu) == bin && (sh0.cidx[lo] & 0x80000000u);
+  };
+  auto pair_code = [&](float2 x, uint32_t bin) -> uint32_t {
+    if (dropped(x, bin)) return 0u;
+    return encode_code(a.q, x.x) | (encode_code(a.q, x.y) << 16);
+  };
+
+  // ---- 6. bin-ordered code array in CTA 0's shared memory (its FFT buffer)
+  uint32_t* arr = reinterpret_cast<uint32_t*>(sh.buf);       // CTA 0 only
+  uint32_t* arr0 = reinterpret_cast<uint32_t*>(sh0.buf);
+  if (r == 0) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t ba = BIN_A(j), bb = BIN_B(j);
+      arr[pad(ba)] = pair_code(va[j], ba);
+      arr[pad(ba + 1)] = 0u;        // odd neighbour, filled by CTA 1 if non-zero
+      arr[pad(bb)] = pair_code(vb[j], bb);
+      arr[pad(bb + 1)] = 0u;
+    }
+    if (special) arr[pad(kN)] = pair_code(xn, kN);
+  }
+  cluster.sync();
+  if (r == 1) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t ca = pair_code(va[j], BIN_A(j));
+      const uint32_t cb = pair_code(vb[j], BIN_B(j));
+      if (ca) arr0[pad(BIN_A(j))] = ca;
+      if (cb) arr0[pad(BIN_B(j))] = cb;
+    }
+  }
+  cluster.sync();
+  if (r == 1) return;
+#undef BIN_A
+#undef BIN_B
+
+  // ---- 7. CTA 0 packs: thread t owns bins [64t, 64t+64) (+ bin N for t = 511)
+  const int N = a.q.n_bits;
+  const uint32_t b0 = 64u * tid;
+  const uint32_t nb = (tid == kThreads - 1) ? 65u : 64u;
+  uint32_t words[5] = {0, 0, 0, 0, 0};
+  for (uint32_t j = 0; j < nb; ++j) {
+    const uint32_t pc = arr[pad(b0 + j)];
+    const uint32_t bits = ((pc & 0xFFFFu) ? 1u : 0u) | ((pc >> 16) ? 2u : 0u);
+    words[j >> 4] |= bits << (2 * (j & 15));
+  }
+  uint32_t cnt = 0;
+  const uint32_t nw = (nb + 15) / 16;
+#pragma unroll
+  for (int w = 0; w < 5; ++w) cnt += __popc(words[w]);
+  uint32_t* seg = reinterpret_cast<uint32_t*>(a.message + ci.seg_off);
+  uint32_t* bm = seg + kSegHeader / 4;
+  for (uint32_t w = 0; w < nw; ++w) bm[4 * tid + w] = ballot_to_wire(words[w]);
+  if (tid == kThreads - 1) {
+    const uint32_t pad_words = (ci.code_off - kSegHeader) / 4;
+    for (uint32_t w = kBmWords; w < pad_words; ++w) bm[w] = 0u;
+  }
+  uint32_t total;
+  const uint32_t base = block_exclusive_scan<kThreads>(cnt, sh.scan, total);
+  // emit this thread's codes: bits [base*N, (base+cnt)*N) of the stream
+  uint64_t bitpos = (uint64_t)base * N;
+  uint32_t wcur = (uint32_t)(bitpos >> 5);
+  uint32_t fill = (uint32_t)(bitpos & 31u);
+  const bool shared_head = fill != 0;
+  bool first = true;
+  uint64_t acc = 0;
+  bool overflow = false;
+  auto emit = [&](uint32_t word, bool partial) {
+    if (wcur >= ci.code_cap) { overflow = true; return; }
+    if (partial || (first && shared_head)) atomicOr(&codes_g[wcur], word);
+    else codes_g[wcur] = word;
+  };
+  for (uint32_t w = 0; w < nw; ++w) {
+    uint32_t bits = words[w];
+    while (bits) {
+      const uint32_t pos = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const uint32_t bin = b0 + 16 * w + (pos >> 1);
+      const uint32_t pc = arr[pad(bin)];
+      const uint32_t code = (pos & 1) ? (pc >> 16) : (pc & 0xFFFFu);
+      acc |= (uint64_t)code << fill;
+      fill += N;
+      if (fill >= 32) {
+        emit((uint32_t)acc, false);
+        first = false;
+        acc >>= 32;
+        fill -= 32;
+        ++wcur;
+      }
+    }
+  }
+  if (fill > 0 && cnt > 0) emit((uint32_t)acc, true);
+  if (tid == 0) {
+    seg[0] = total;
+    seg[1] = 0; seg[2] = 0; seg[3] = 0;
+  }
+  if (overflow) atomicOr(a.flags, FGC_FLAG_CAPACITY);
 }
-fgc_status launch_fused_inverse(const FusedTables*, const ChunkInfo*, uint32_t, uint32_t, const float2*, float*,
-                                cudaStream_t) {
-  return FGC_ERR_UNSUPPORTED;
+
+// ------------------------------------------------------------------ decode
+
+struct DecodeArgs {
+  const ChunkInfo* chunks;
+  uint32_t first;
+  const uint8_t* messages;
+  int W;
+  uint64_t stride;
+  Weights wts;
+  QuantParams q;
+  float* out;
+  const float2* thi;
+  const float2* tlo;
+  const float2* spectrum;     // dense-spectrum mode (debug hook), else null
+};
+
+struct __align__(16) DecodeShared {
+  float2 y[kPadded + 64];
+  float2 thi[256], tlo[256];
+  uint32_t bm[kBmWords + 3];
+  uint32_t pref[kBmWords + 3];
+  uint32_t scan[40];
+};
+
+// Add the contributions of bin b's (weighted) value X to Y_r.
+__device__ __forceinline__ void scatter_bin(DecodeShared& sh, uint32_t r, uint32_t b, float2 X) {
+  const float2 wb = tw(sh.thi, sh.tlo, b);                      // W_L^b
+  float2 cA = make_float2(0.5f * (1.0f + wb.y), 0.5f * wb.x);   // (1 + i W_L^-b)/2
+  float2 cB = make_float2(0.5f * (1.0f - wb.y), 0.5f * wb.x);   // (1 + i W_L^b)/2
+  if (r) {
+    const float2 w2 = tw(sh.thi, sh.tlo, 2u * b);               // W_N^b
+    cA = cmulc(cA, w2);                                         // * W_N^-b
+    cB = cmul(cB, w2);                                          // * W_N^b
+  }
+  if (b < kN) {
+    float2& y = sh.y[pad(b & (kM - 1))];
+    const float2 c = cmul(cA, X);
+    y.x += c.x;
+    y.y += c.y;
+  }
+  if (b > 0) {
+    float2& y = sh.y[pad((kN - b) & (kM - 1))];
+    const float2 c = cmul(cB, make_float2(X.x, -X.y));
+    y.x += c.x;
+    y.y += c.y;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  DecodeShared& sh = *reinterpret_cast<DecodeShared*>(smem_raw);
+  const uint32_t r = blockIdx.x & 1u;
+  const uint32_t chunk = a.first + blockIdx.x / 2;
+  const ChunkInfo ci = a.chunks[chunk];
+  const uint32_t tid = threadIdx.x;
+  if (tid < 256) {
+    sh.thi[tid] = a.thi[tid];
+    sh.tlo[tid] = a.tlo[tid];
+  }
+  for (uint32_t e = tid; e < kPadded + 64; e += kThreads) sh.y[e] = make_float2(0.f, 0.f);
+  __syncthreads();
+
+  if (a.spectrum) {
+    // dense spectrum input: four quarters, one bin per thread per step
+    const float2* X = a.spectrum + ci.bin_off;
+    for (uint32_t q = 0; q < 4; ++q) {
+      const uint32_t lo = q * (kN / 4), hi = (q == 3) ? kBins : (q + 1) * (kN / 4);
+      for (uint32_t b = lo + tid; b < hi; b += kThreads) {
+        float2 x = X[b];
+        if (b == 0 || b == kN) x.y = 0.f;
+        scatter_bin(sh, r, b, x);
+      }
+      __syncthreads();
+    }
+  } else {
+    const int N = a.q.n_bits;
+    for (int w = 0; w < a.W; ++w) {
+      const uint8_t* seg = a.messages + (uint64_t)w * a.stride + ci.seg_off;
+      const uint32_t* bmg = reinterpret_cast<const uint32_t*>(seg + kSegHeader);
+      const uint32_t* cw = reinterpret_cast<const uint32_t*>(seg + ci.code_off);
+      // bitmap (slot order) + exclusive popcount prefix per word
+      uint32_t loc[5], local = 0;
+      const uint32_t w0 = 4 * tid, nw = (tid == kThreads - 1) ? 5u : 4u;
+#pragma unroll
+      for (uint32_t k = 0; k < 5; ++k) {
+        loc[k] = 0;
+        if (k < nw) {
+          loc[k] = ballot_to_wire(bmg[w0 + k]);
+          local += __popc(loc[k]);
+        }
+      }
+      uint32_t tot;
+      uint32_t base = block_exclusive_scan<kThreads>(local, sh.scan, tot);
+#pragma unroll
+      for (uint32_t k = 0; k < 5; ++k) {
+        if (k < nw) {
+          sh.bm[w0 + k] = loc[k];
+          sh.pref[w0 + k] = base;
+          base += __popc(loc[k]);
+        }
+      }
+      __syncthreads();
+      const float wt = a.wts.w[w];
+      for (uint32_t q = 0; q < 4; ++q) {
+        const uint32_t nwq = (q == 3 && tid == 0) ? 2u : 1u;
+        for (uint32_t e = 0; e < nwq; ++e) {
+          const uint32_t word = (e == 0) ? q * 512u + tid : kBmWords - 1;
+          uint32_t sw = sh.bm[word];
+          if (!sw) continue;
+          const uint32_t pb = sh.pref[word];
+          while (sw) {
+            const uint32_t pos = __ffs(sw) - 1;          // lowest set slot bit
+            const uint32_t jb = pos >> 1;
+            const uint32_t bits = (sw >> (2 * jb)) & 3u;
+            sw &= ~(3u << (2 * jb));
+            uint32_t rank = pb + __popc(sh.bm[word] & ((1u << (2 * jb)) - 1u));
+            float re = 0.f, im = 0.f;
+            if (bits & 1u) { re = decode_code(a.q, read_bits(cw, (uint64_t)rank * N, N)); ++rank; }
+            if (bits & 2u) im = decode_code(a.q, read_bits(cw, (uint64_t)rank * N, N));
+            const uint32_t b = word * 16u + jb;
+            if (b == 0 || b == kN) im = 0.f;
+            scatter_bin(sh, r, b, make_float2(re * wt, im * wt));
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+
+  // inverse 16384-point FFT of Y_r, natural-order output
+  float2 v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = sh.y[pad(tid + 512u * j)];
+  __syncthreads();
+  fft_pass12<true>(v, sh.y, sh.thi, sh.tlo);
+  __syncthreads();
+  const float scale = 1.0f / (float)kN;
+  float* out = a.out + ci.in_off;
+  for (uint32_t c = 0; c < 2; ++c) {
+    const uint32_t k = tid + 512u * c;
+    float2 o[16];
+    fft_pass3<true>(k, sh.y, o, sh.thi, sh.tlo);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const uint32_t p = k + 1024u * m;
+      *reinterpret_cast<float2*>(out + 4ull * p + 2 * r) = make_float2(o[m].x * scale, o[m].y * scale);
+    }
+  }
+}
+
+template <class K>
+fgc_status set_smem(K kernel, size_t bytes) {
+  FGC_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return FGC_OK;
+}
+
+}  // namespace
+
+bool fused_available() { return true; }
+
+fgc_status fused_tables_init(FusedTables** t, cudaStream_t s) {
+  FusedTables* ft = new FusedTables();
+  cudaError_t e = cudaMalloc(&ft->thi, 256 * sizeof(float2));
+  if (e == cudaSuccess) e = cudaMalloc(&ft->tlo, 256 * sizeof(float2));
+  if (e != cudaSuccess) {
+    fused_tables_free(ft);
+    return cuda_check(e, "cudaMalloc");
+  }
+  k_init_tables<<<1, 256, 0, s>>>(ft->thi, ft->tlo);
+  FGC_LAUNCHED(1);
+  static bool attrs = false;
+  if (!attrs) {
+    FGC_TRY(set_smem(k_fused_compress<float, false>, sizeof(CompressShared)));
+    FGC_TRY(set_smem(k_fused_compress<double, false>, sizeof(CompressShared)));
+    FGC_TRY(set_smem(k_fused_compress<float, true>, sizeof(CompressShared)));
+    FGC_TRY(set_smem(k_fused_compress<double, true>, sizeof(CompressShared)));
+    FGC_TRY(set_smem(k_fused_decode, sizeof(DecodeShared)));
+    attrs = true;
+  }
+  *t = ft;
+  return FGC_OK;
+}
+
+void fused_tables_free(FusedTables* t) {
+  if (!t) return;
+  cudaFree(t->thi);
+  cudaFree(t->tlo);
+  delete t;
+}
+
+static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first,
+                                       uint32_t count, const void* grad, int dtype, int half_pass,
+                                       const QuantParams& q, uint8_t* message, uint32_t* flags, uint32_t* fb,
+                                       float2* fb_spec, float2* dbg, cudaStream_t s) {
+  if (!count) return FGC_OK;
+  CompressArgs a{d_chunks, first, grad, half_pass, q, message, flags, t->thi, t->tlo, fb, fb_spec, dbg};
+  const size_t smem = sizeof(CompressShared);
+  const dim3 grid(2 * count), block(kThreads);
+  if (dbg) {
+    if (dtype == FGC_DTYPE_F64) k_fused_compress<double, true><<<grid, block, smem, s>>>(a);
+    else k_fused_compress<float, true><<<grid, block, smem, s>>>(a);
+  } else {
+    if (dtype == FGC_DTYPE_F64) k_fused_compress<double, false><<<grid, block, smem, s>>>(a);
+    else k_fused_compress<float, false><<<grid, block, smem, s>>>(a);
+  }
+  FGC_LAUNCHED(1);
+  return FGC_OK;
+}
+
+fgc_status launch_fused_compress(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                                 const void* grad, int dtype, int half_pass, const QuantParams& q,
+                                 uint8_t* message, uint32_t* flags, uint32_t* fb, float2* fb_spec,
+                                 cudaStream_t s) {
+  if (q.n_bits > 16) {
+    set_error("fused kernels take N <= 16");
+    return FGC_ERR_UNSUPPORTED;
+  }
+  return launch_compress_impl(t, d_chunks, first, count, grad, dtype, half_pass, q, message, flags, fb, fb_spec,
+                              nullptr, s);
+}
+
+fgc_status launch_fused_spectrum(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                                 const void* grad, int dtype, int half_pass, float2* spectrum, uint32_t* flags,
+                                 cudaStream_t s) {
+  QuantParams q{};
+  q.n_bits = 8;
+  return launch_compress_impl(t, d_chunks, first, count, grad, dtype, half_pass, q, nullptr, flags, nullptr,
+                              nullptr, spectrum, s);
+}
+
+fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                               const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
+                               const QuantParams& q, float* out, cudaStream_t s) {
+  if (!count) return FGC_OK;
+  DecodeArgs a{d_chunks, first, messages, W, stride, wts, q, out, t->thi, t->tlo, nullptr};
+  k_fused_decode<<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
+  FGC_LAUNCHED(1);
+  return FGC_OK;
+}
+
+fgc_status launch_fused_inverse(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                                const float2* spectrum, float* out, cudaStream_t s) {
+  if (!count) return FGC_OK;
+  DecodeArgs a{};
+  a.chunks = d_chunks;
+  a.first = first;
+  a.out = out;
+  a.thi = t->thi;
+  a.tlo = t->tlo;
+  a.spectrum = spectrum;
+  a.W = 0;
+  k_fused_decode<<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
+  FGC_LAUNCHED(1);
+  return FGC_OK;
 }
 
 }  // namespace fgc

@@ -1,0 +1,136 @@
+// Register-resident FFT building blocks for the fused 65536-sample kernels.
+//
+// A CTA of 512 threads transforms M = 16384 complex points held 32 per
+// thread in registers: three Stockham radix passes (32 x 32 x 16) with two
+// shared-memory transposes between them (padded one float2 per 32 so every
+// transpose is bank-conflict free).  Twiddles come from a two-level table of
+// W_65536 = exp(-2 pi i / 65536) in shared memory (256 + 256 entries built in
+// float64), so every twiddle costs one complex multiply.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fgc_device.cuh"
+
+namespace fgc {
+namespace ff {
+
+constexpr int kThreads = 512;       // CTA size of the fused kernels
+constexpr uint32_t kM = 16384;      // per-CTA transform length
+constexpr uint32_t kN = 32768;      // complex length of a 65536-real chunk
+constexpr uint32_t kL = 65536;      // chunk length
+constexpr uint32_t kPadded = kM + kM / 32;
+
+__device__ __forceinline__ uint32_t pad(uint32_t e) { return e + (e >> 5); }
+
+// cos / sin (2 pi m / 32), m = 0..15
+__device__ constexpr float kC32[16] = {1.0f, 0.98078528040323043f, 0.92387953251128674f, 0.83146961230254524f,
+                                        0.70710678118654752f, 0.55557023301960222f, 0.38268343236508977f,
+                                        0.19509032201612826f, 0.0f, -0.19509032201612826f, -0.38268343236508977f,
+                                        -0.55557023301960222f, -0.70710678118654752f, -0.83146961230254524f,
+                                        -0.92387953251128674f, -0.98078528040323043f};
+__device__ constexpr float kS32[16] = {0.0f, 0.19509032201612826f, 0.38268343236508977f, 0.55557023301960222f,
+                                        0.70710678118654752f, 0.83146961230254524f, 0.92387953251128674f,
+                                        0.98078528040323043f, 1.0f, 0.98078528040323043f, 0.92387953251128674f,
+                                        0.83146961230254524f, 0.70710678118654752f, 0.55557023301960222f,
+                                        0.38268343236508977f, 0.19509032201612826f};
+
+constexpr int bitrev(int x, int bits) {
+  int r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1) << (bits - 1 - i);
+  return r;
+}
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+
+// d * W_32^m (forward: exp(-2 pi i m/32); INV: conjugate), m compile-time.
+template <int M32, bool INV>
+__device__ __forceinline__ float2 tw32(float2 d) {
+  if constexpr (M32 == 0) {
+    return d;
+  } else if constexpr (M32 == 8) {
+    return INV ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);
+  } else {
+    constexpr float c = kC32[M32];
+    constexpr float s = INV ? kS32[M32] : -kS32[M32];
+    return make_float2(__fmaf_rn(d.x, c, -d.y * s), __fmaf_rn(d.x, s, d.y * c));
+  }
+}
+
+template <int S, int A, int R, bool INV>
+__device__ __forceinline__ void dif_stage_inner(float2 (&v)[R]) {
+  if constexpr (A < S) {
+#pragma unroll
+    for (int b = 0; b < R; b += 2 * S) {
+      const float2 x = v[b + A], y = v[b + A + S];
+      v[b + A] = make_float2(x.x + y.x, x.y + y.y);
+      v[b + A + S] = tw32<A * (16 / S), INV>(make_float2(x.x - y.x, x.y - y.y));
+    }
+    dif_stage_inner<S, A + 1, R, INV>(v);
+  }
+}
+
+template <int S, int R, bool INV>
+__device__ __forceinline__ void dif_stages(float2 (&v)[R]) {
+  if constexpr (S >= 1) {
+    dif_stage_inner<S, 0, R, INV>(v);
+    dif_stages<S / 2, R, INV>(v);
+  }
+}
+
+// In-place radix-2 DIF DFT of R <= 32 points; result in bit-reversed order:
+// v[bitrev(m)] = X[m].
+template <int R, bool INV>
+__device__ __forceinline__ void dft(float2 (&v)[R]) {
+  static_assert(R == 16 || R == 32, "R");
+  dif_stages<R / 2, R, INV>(v);
+}
+
+// W_65536^m from the two-level table (m taken mod 65536).
+__device__ __forceinline__ float2 tw(const float2* thi, const float2* tlo, uint32_t m) {
+  return cmul(thi[(m >> 8) & 255u], tlo[m & 255u]);
+}
+__device__ __forceinline__ float2 twc(const float2* thi, const float2* tlo, uint32_t m, bool inv) {
+  float2 w = tw(thi, tlo, m);
+  if (inv) w.y = -w.y;
+  return w;
+}
+
+// Passes 1 and 2 of the 16384-point transform.  On entry v[j] holds
+// x[i + 512 j]; on exit the pass-2 output sits in `buf` (padded layout),
+// ready for pass 3 (caller syncs).
+template <bool INV>
+__device__ __forceinline__ void fft_pass12(float2 (&v)[32], float2* buf, const float2* thi, const float2* tlo) {
+  const uint32_t i = threadIdx.x;
+  dft<32, INV>(v);
+#pragma unroll
+  for (int m = 0; m < 32; ++m) buf[pad(32 * i + m)] = v[bitrev(m, 5)];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = buf[pad(i + 512 * j)];
+  const uint32_t k = i & 31u;
+#pragma unroll
+  for (int j = 1; j < 32; ++j) v[j] = cmul(v[j], twc(thi, tlo, 64u * j * k, INV));   // W_1024^{jk}
+  dft<32, INV>(v);
+  const uint32_t base = (i >> 5) * 1024u + k;
+  __syncthreads();                      // every pass-2 read is done before the writes
+#pragma unroll
+  for (int m = 0; m < 32; ++m) buf[pad(base + 32 * m)] = v[bitrev(m, 5)];
+}
+
+// Pass 3 for one column k: reads x[k + 1024 j] (j < 16) from buf, applies
+// W_16384^{jk}, and leaves out[m] = X[k + 1024 m] in natural order.
+template <bool INV>
+__device__ __forceinline__ void fft_pass3(uint32_t k, const float2* buf, float2 (&out)[16], const float2* thi,
+                                          const float2* tlo) {
+  float2 v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = buf[pad(k + 1024u * j)];
+#pragma unroll
+  for (int j = 1; j < 16; ++j) v[j] = cmul(v[j], twc(thi, tlo, 4u * j * k, INV));    // W_16384^{jk}
+  dft<16, INV>(v);
+#pragma unroll
+  for (int m = 0; m < 16; ++m) out[m] = v[bitrev(m, 4)];
+}
+
+}  // namespace ff
+}  // namespace fgc

@@ -45,6 +45,7 @@ struct fgc_plan {
   ChunkInfo* d_chunks = nullptr;
   float2* d_spec = nullptr;
   uint64_t* d_scratch = nullptr;
+  uint32_t* d_fb = nullptr;          // per-chunk fused-kernel fallback flags
   FusedTables* fused = nullptr;
   uint32_t fused_first = 0, fused_count = 0;     // chunk range taken by fused kernels
 };
@@ -128,7 +129,8 @@ extern "C" fgc_status fgc_plan_create(const fgc_codec_desc* desc, fgc_plan** out
     c.bins = c.L / 2 + 1;
     c.first = 0;
     c.count = (uint32_t)full;
-    c.fused = fused_available() && fused_enabled() && c.L == 65536 && d.mode == FGC_MODE_COUNT;
+    c.fused = fused_available() && fused_enabled() && c.L == 65536 && d.mode == FGC_MODE_COUNT &&
+              !d.passthrough && d.quant.n_bits <= 16;
     p->classes.push_back(c);
   }
   if (tail) {
@@ -196,6 +198,10 @@ extern "C" fgc_status fgc_plan_create(const fgc_codec_desc* desc, fgc_plan** out
   if ((e = cudaMalloc(&p->d_spec, sizeof(float2) * p->spec_bins)) != cudaSuccess) return fail(cuda_check(e, "cudaMalloc"));
   if ((e = cudaMalloc(&p->d_scratch, sizeof(uint64_t) * (p->n_chunks + 1))) != cudaSuccess)
     return fail(cuda_check(e, "cudaMalloc"));
+  if ((e = cudaMalloc(&p->d_fb, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
+    return fail(cuda_check(e, "cudaMalloc"));
+  if ((e = cudaMemset(p->d_fb, 0, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
+    return fail(cuda_check(e, "cudaMemset"));
   for (RealClass& rc : p->classes) {
     if (rc.fused) {
       fgc_status st = fused_tables_init(&p->fused, s);
@@ -219,6 +225,7 @@ extern "C" void fgc_plan_destroy(fgc_plan* p) {
   cudaFree(p->d_chunks);
   cudaFree(p->d_spec);
   cudaFree(p->d_scratch);
+  cudaFree(p->d_fb);
   delete p;
 }
 
@@ -277,9 +284,13 @@ extern "C" fgc_status fgc_compress(fgc_plan* p, const void* grad, int dtype, uin
   if (!p || !grad || !message || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
   FGC_TRY(check_mode(p));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (p->fused_count)
+  if (p->fused_count) {
     FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, p->fused_first, p->fused_count, grad, dtype,
-                                  p->desc.half_pass, p->q, message, flags, s));
+                                  p->desc.half_pass, p->q, message, flags, p->d_fb, p->d_spec, s));
+    // degenerate chunks the fused select handed back (flag set, spectrum in d_spec)
+    FGC_TRY(launch_select_pack(p->d_chunks, p->fused_first, p->fused_count, p->d_spec, 0, p->q, message, nullptr,
+                               flags, s, p->d_fb));
+  }
   FGC_TRY(forward_generic(p, grad, dtype, p->d_spec, flags, s, false));
   // generic chunks are the ones outside [fused_first, fused_first + fused_count)
   for (RealClass& rc : p->classes) {

@@ -72,6 +72,18 @@ def decode_spectrum(messages: list, weights=None) -> np.ndarray:
     return out.cpu().numpy().view(np.complex64).reshape(-1)
 
 
+def decode_average(messages: list, weights=None) -> np.ndarray:
+    """fgc_decode_average over stacked device messages (one plan)."""
+    plan, _ = messages[0].device_message()
+    stacked = torch.cat([m.device_message()[1] for m in messages])
+    W = len(messages)
+    out = torch.empty(int(plan.desc.n), dtype=torch.float32, device=stacked.device)
+    w = None if weights is None else np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+    _lib.check(_lib.lib.fgc_decode_average(plan.handle, stacked.data_ptr(), W, plan.message_bytes,
+                                           None if w is None else w.ctypes.data, out.data_ptr(), D.stream()))
+    return out.cpu().numpy()
+
+
 def inverse_spectrum(spectrum, n: int, config: CodecConfig) -> np.ndarray:
     plan = plan_for(n, config)
     sp = np.ascontiguousarray(np.asarray(spectrum, dtype=np.complex64)).view(np.float32)

@@ -255,6 +255,51 @@ def test_decode_average_multi_message_exact_messages():
     assert rel_l2(got, ref) <= 1e-5
 
 
+def _oracle_message_from_gpu_coeffs(g, cfg, n, chunk, theta, q):
+    spec = debug.forward_spectrum(g, cfg)
+    chunks, pos = [], 0
+    for L in O.chunk_lengths(n, chunk):
+        b = L // 2 + 1
+        chunks.append(O.encode_spectrum(spec[pos:pos + b], L, theta, "count", lat_of(q))[1])
+        pos += b
+    return O.Message(n, chunk, float(np.float32(theta)), "count", False, lat_of(q), chunks)
+
+
+@pytest.mark.parametrize("theta", [0.0, 0.5, 0.9, 0.99, 1.0])
+def test_fused_degenerate_and_mixed_chunks(theta):
+    """Chunks that force every branch of the fused selection: all zero,
+    constant (one non-zero bin), impulses (flat spectrum: heavy ties),
+    tiny values (fallback to the exact generic select), random."""
+    rng = np.random.default_rng(11)
+    L = 65536
+    parts = [np.zeros(L), np.full(L, 0.25), np.zeros(L), (rng.standard_normal(L) * 1e-30),
+             rng.standard_normal(L) * 1e-2, rng.standard_normal(L) * 1e-2]
+    parts[2][::4096] = 1.0
+    parts[5][::7] = 0.0
+    g = np.concatenate(parts).astype(np.float32)
+    q = F.calibrate([g], 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta), q)
+    msg = F.compress(g, cfg)
+    om = _oracle_message_from_gpu_coeffs(g, cfg, g.size, L, theta, q)
+    assert F.serialize(msg) == O.to_wire(om)
+
+
+@pytest.mark.parametrize("W", [1, 3, 8])
+def test_fused_decode_average_matches_oracle(W):
+    rng = np.random.default_rng(12 + W)
+    n, chunk = 65536 * 3 + 777, 65536
+    rows = (rng.standard_normal((W, n)) * 1e-2).astype(np.float32)
+    q = F.calibrate([rows[0]], 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.9), q, chunk_size=chunk)
+    w = rng.random(W)
+    msgs = [F.compress(r, cfg) for r in rows]
+    got = debug.decode_average(msgs, w)
+    ref = sum(wi * O.decompress(O.from_wire(F.serialize(m))) for wi, m in zip(w, msgs))
+    assert rel_l2(got, ref) <= 1e-5
+    # deterministic: identical bits on a second run
+    np.testing.assert_array_equal(got, debug.decode_average(msgs, w))
+
+
 # ---------------------------------------------------------------- wire
 
 def test_golden_fixtures_round_trip(golden):
