@@ -39,8 +39,10 @@ def q_of(rec):
 
 
 def rel_l2(a, b):
-    a = np.asarray(a, dtype=np.float64)
-    b = np.asarray(b, dtype=np.float64)
+    a = np.asarray(a)
+    b = np.asarray(b)
+    a = a.astype(np.complex128 if np.iscomplexobj(a) else np.float64)
+    b = b.astype(np.complex128 if np.iscomplexobj(b) else np.float64)
     nb = np.linalg.norm(b)
     return np.linalg.norm(a - b) / (nb if nb else 1.0)
 
