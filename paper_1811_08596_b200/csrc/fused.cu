@@ -16,12 +16,12 @@
 //   radix select on a float32 proxy of |X|^2 (histograms merged through
 //   DSMEM), with numpy's exact float64 cabs key and the stable index
 //   tie-break applied to the few bins whose proxy is too close to call.
-//   Codes (quantizer.py:217-236) are gathered bin-ordered into CTA 0's shared
-//   memory (CTA 1 stores its non-zero pairs remotely) and CTA 0 emits the
-//   MSB-first bitmap and the LSB-first packed code stream (packer.py,
-//   quantizer.pack_codes) straight into the device message segment.
-//   Degenerate chunks (all proxies tiny, or > kCand undecided bins) are
-//   handed to the generic select kernel via a per-chunk flag.
+//   Codes (quantizer.py:217-236) are gathered bin-ordered into two halves,
+//   one per CTA (each CTA stores the other's non-zero pairs remotely), and
+//   each CTA emits its half of the MSB-first bitmap and of the LSB-first
+//   packed code stream (packer.py, quantizer.pack_codes) straight into the
+//   device message segment.  Degenerate chunks (all proxies tiny, or > kCand
+//   undecided bins) are handed to the generic select kernel via a flag.
 //
 // decode (k_fused_decode, 2 CTAs per chunk, 512 threads)
 //   CTA r builds Y_r (16384 complex, shared memory) directly from the W
@@ -36,6 +36,8 @@
 #include <cuda_fp16.h>
 #include <math.h>
 
+#include <type_traits>
+
 #include "fgc_device.cuh"
 #include "fgc_internal.h"
 #include "fused_fft.cuh"
@@ -45,8 +47,9 @@ namespace cg = cooperative_groups;
 namespace fgc {
 
 struct FusedTables {
-  float2* thi = nullptr;   // W_65536^(256 h), h < 256
-  float2* tlo = nullptr;   // W_65536^l, l < 256
+  float2* thi = nullptr;     // W_65536^(256 h), h < 256
+  float2* tlo = nullptr;     // W_65536^l, l < 256
+  float2* t1024 = nullptr;   // W_1024^m, m < 1024
 };
 
 namespace {
@@ -54,16 +57,29 @@ namespace {
 using namespace ff;
 
 constexpr int kCand = 1024;
-constexpr uint32_t kBins = kN + 1;           // 32769
-constexpr uint32_t kBmWords = (2 * kBins + 31) / 32;   // 2049
+constexpr uint32_t kBins = kN + 1;                     // 32769
+constexpr uint32_t kBmWords = (2 * kBins + 31) / 32;  // 2049
+constexpr uint32_t kHalfBins = kN / 2;                 // 16384: pack split point
 
-__global__ void k_init_tables(float2* thi, float2* tlo) {
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+__global__ void k_init_tables(float2* thi, float2* tlo, float2* t1024) {
   const int i = threadIdx.x;
   double s, c;
-  sincospi(-2.0 * (double)(256 * i) / 65536.0, &s, &c);
-  thi[i] = make_float2((float)c, (float)s);
-  sincospi(-2.0 * (double)i / 65536.0, &s, &c);
-  tlo[i] = make_float2((float)c, (float)s);
+  if (i < 256) {
+    sincospi(-2.0 * (double)(256 * i) / 65536.0, &s, &c);
+    thi[i] = make_float2((float)c, (float)s);
+    sincospi(-2.0 * (double)i / 65536.0, &s, &c);
+    tlo[i] = make_float2((float)c, (float)s);
+  }
+  sincospi(-2.0 * (double)i / 1024.0, &s, &c);
+  t1024[i] = make_float2((float)c, (float)s);
 }
 
 // ------------------------------------------------------------------ loads
@@ -71,19 +87,19 @@ __global__ void k_init_tables(float2* thi, float2* tlo) {
 template <class T> struct In;
 template <> struct In<float> {
   __device__ static float2 get(const float* g, uint64_t e, int half, uint32_t& bad) {
-    float2 v = *reinterpret_cast<const float2*>(g + e);
-    if (!isfinite(v.x) || !isfinite(v.y)) { bad |= FGC_FLAG_NONFINITE; v = make_float2(0.f, 0.f); }
+    float2 v = __ldg(reinterpret_cast<const float2*>(g + e));
+    bad |= (isfinite(v.x) && isfinite(v.y)) ? 0u : FGC_FLAG_NONFINITE;
     if (half) {
       v.x = __half2float(__float2half_rn(v.x));
       v.y = __half2float(__float2half_rn(v.y));
-      if (isinf(v.x) || isinf(v.y)) bad |= FGC_FLAG_HALF_OVERFLOW;
+      bad |= (isinf(v.x) || isinf(v.y)) ? FGC_FLAG_HALF_OVERFLOW : 0u;
     }
     return v;
   }
 };
 template <> struct In<double> {
   __device__ static float2 get(const double* g, uint64_t e, int half, uint32_t& bad) {
-    const double2 d = *reinterpret_cast<const double2*>(g + e);
+    const double2 d = __ldg(reinterpret_cast<const double2*>(g + e));
     if (!isfinite(d.x) || !isfinite(d.y)) { bad |= FGC_FLAG_NONFINITE; return make_float2(0.f, 0.f); }
     float2 v;
     if (half) {
@@ -97,6 +113,15 @@ template <> struct In<double> {
   }
 };
 
+// encode_code specialised for N <= 16 (no passthrough branch)
+__device__ __forceinline__ uint32_t enc16(const QuantParams& q, float x) {
+  const float a = fabsf(x);
+  const uint32_t op = (__float_as_uint(fminf(a, q.pos_cap)) >> q.shift) - q.pbase + 1u;
+  const uint32_t on = (__float_as_uint(fminf(a, q.neg_cap)) >> q.shift) - q.pbase + 1u;
+  const uint32_t c = (x > 0.0f) ? min(op, q.npos) : q.npos + min(on, q.nneg);
+  return (a < q.eps) ? 0u : c;
+}
+
 // ------------------------------------------------------------------ compress
 
 struct CompressArgs {
@@ -109,22 +134,25 @@ struct CompressArgs {
   uint32_t* flags;
   const float2* thi;
   const float2* tlo;
+  const float2* t1024;
   uint32_t* fb;          // per-chunk fallback flag (indexed by chunk id)
   float2* fb_spec;       // chunk-major spectrum scratch for fallback chunks
   float2* dbg_spec;      // debug hook: write the spectrum and stop
 };
 
 struct __align__(16) CompressShared {
-  float2 buf[kPadded + 64];          // FFT transposes, then the bin-ordered code array
+  float2 buf[kPadded + 64];          // FFT transposes / 4 sub-histograms / bin-ordered code half
   float2 thi[256], tlo[256];
-  uint32_t hist[2048];
+  float2 t1024[1024];
+  uint32_t hist[2048];               // merged histogram of this CTA (read by the peer)
   uint32_t scan[40];
   unsigned long long ckey[kCand];    // CTA 0: undecided bins (exact key, bin)
   uint32_t cidx[kCand];
   uint32_t ccount;                   // CTA 0: number of undecided bins
   uint32_t below;                    // per CTA: bins certainly dropped
   uint32_t anynz;                    // per CTA: any non-zero coefficient
-  uint32_t fbin, fbelow;             // find_bucket result
+  uint32_t total;                    // per CTA: codes in its half of the stream
+  uint32_t fbin, fbelow;             // merged_bucket result
   int mode;                          // CTA 0's decision, read by CTA 1
   uint32_t need;
 };
@@ -159,12 +187,15 @@ __device__ void merged_bucket(CompressShared& sh, const uint32_t* peer_hist, uin
   below = sh.fbelow;
 }
 
-// Histogram add with warp aggregation of equal buckets.
-__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t bucket, bool active) {
-  const uint32_t am = __ballot_sync(0xffffffffu, active);
-  if (!active) return;
-  const uint32_t peers = __match_any_sync(am, bucket);
-  if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&hist[bucket], (uint32_t)__popc(peers));
+// sub-histograms (one per warp quad) in the free FFT buffer -> merged hist
+__device__ __forceinline__ uint32_t* subhist(CompressShared& sh) { return reinterpret_cast<uint32_t*>(sh.buf); }
+__device__ __forceinline__ void zero_subhist(CompressShared& sh) {
+  uint4* s = reinterpret_cast<uint4*>(sh.buf);
+  for (uint32_t e = threadIdx.x; e < 4 * 2048 / 4; e += kThreads) s[e] = make_uint4(0, 0, 0, 0);
+}
+__device__ __forceinline__ void merge_subhist(CompressShared& sh) {
+  const uint32_t* s = subhist(sh);
+  for (uint32_t b = threadIdx.x; b < 2048; b += kThreads) sh.hist[b] = s[b] + s[2048 + b] + s[4096 + b] + s[6144 + b];
 }
 
 template <class T, bool DEBUG>
@@ -178,12 +209,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   const ChunkInfo ci = a.chunks[chunk];
   CompressShared& sh0 = *cluster.map_shared_rank(&sh, 0);
   CompressShared& shp = *cluster.map_shared_rank(&sh, r ^ 1);
+  const QuantParams q = a.q;
 
   if (tid < 256) {
     sh.thi[tid] = a.thi[tid];
     sh.tlo[tid] = a.tlo[tid];
   }
-  for (uint32_t b = tid; b < 2048; b += kThreads) sh.hist[b] = 0;
+  sh.t1024[tid] = a.t1024[tid];
+  sh.t1024[tid + 512] = a.t1024[tid + 512];
   if (tid == 0) { sh.ccount = 0; sh.below = 0; sh.anynz = 0; }
   uint32_t* codes_g = reinterpret_cast<uint32_t*>(a.message + ci.seg_off + ci.code_off);
   const uint32_t cap_padded = (ci.code_cap + 3u) & ~3u;
@@ -196,75 +229,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   {
     const T* g = static_cast<const T*>(a.grad) + ci.in_off;
     uint32_t bad = 0;
-#pragma unroll 8
-    for (int j = 0; j < 32; ++j) {
+    const float2 wi = tw(sh.thi, sh.tlo, 2u * tid);          // W_N^tid
+    static_for<0, 32>([&](auto J) {
+      constexpr int j = decltype(J)::value;
       const uint32_t n = tid + 512u * j;
       const float2 z0 = In<T>::get(g, 2ull * n, a.half, bad);
       const float2 z1 = In<T>::get(g, 2ull * (n + kM), a.half, bad);
       if (r == 0) {
         v[j] = make_float2(z0.x + z1.x, z0.y + z1.y);
-      } else {
-        v[j] = cmul(make_float2(z0.x - z1.x, z0.y - z1.y), tw(sh.thi, sh.tlo, 2u * n));   // W_N^n
+      } else {                                              // (z0 - z1) W_N^(tid + 512 j)
+        v[j] = w64mul<j>(cmul(make_float2(z0.x - z1.x, z0.y - z1.y), wi));
       }
-    }
+    });
     if (bad && r == 0) atomicOr(a.flags, bad);
   }
 
   // ---- 2. 16384-point FFT: passes 1, 2 (transposes in smem), pass 3 on two columns
-  fft_pass12<false>(v, sh.buf, sh.thi, sh.tlo);
+  fft_pass12<false>(v, sh.buf, sh.t1024);
   __syncthreads();
-  uint32_t ka, kb;
-  if (r == 0) {
-    ka = tid;
-    kb = tid == 0 ? 512u : 1024u - tid;
-  } else {
-    ka = tid;
-    kb = 1023u - tid;
-  }
+  const bool special = (r == 0 && tid == 0);
+  const uint32_t ka = tid;
+  const uint32_t kb = (r == 0) ? (tid == 0 ? 512u : 1024u - tid) : 1023u - tid;
   float2 va[16], vb[16];
   fft_pass3<false>(ka, sh.buf, va, sh.thi, sh.tlo);
   fft_pass3<false>(kb, sh.buf, vb, sh.thi, sh.tlo);
 
   // ---- 3. real-FFT post-processing in registers: X[k] = (P + conj Q)/2 - i W_L^k (P - conj Q)/2
-  auto r2c = [&](float2 P, float2 Q, uint32_t bin) -> float2 {
+  auto r2c = [](float2 P, float2 Q, float2 w) -> float2 {
     const float2 A = make_float2(P.x + Q.x, P.y - Q.y);
     const float2 B = make_float2(P.x - Q.x, P.y + Q.y);
-    const float2 t = cmul(tw(sh.thi, sh.tlo, bin), make_float2(B.y, -B.x));
+    const float2 t = cmul(w, make_float2(B.y, -B.x));
     return make_float2(0.5f * (A.x + t.x), 0.5f * (A.y + t.y));
   };
   float2 xn = make_float2(0.f, 0.f);      // X[N] (CTA 0, thread 0 only)
-  const bool special = (r == 0 && tid == 0);
   if (!special) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    // bins: va[j] -> (2ka + r) + 2048 j, vb[j] -> (2kb + r) + 2048 j ; W_L^(2048 j) = W_32^j
+    const float2 wA = tw(sh.thi, sh.tlo, 2u * ka + r);
+    const float2 wB = tw(sh.thi, sh.tlo, 2u * kb + r);
+    static_for<0, 16>([&](auto J) {
+      constexpr int j = decltype(J)::value;
       const float2 P = va[j], Q = vb[15 - j];
-      const uint32_t ma = ka + 1024u * j, mb = kb + 1024u * (15 - j);
-      va[j] = r2c(P, Q, 2u * ma + r);
-      vb[15 - j] = r2c(Q, P, 2u * mb + r);
-    }
+      va[j] = r2c(P, Q, w32mul<j>(wA));
+      vb[15 - j] = r2c(Q, P, w32mul<15 - j>(wB));
+    });
   } else {
-    // column 0: pairs j <-> 16-j, self pairs j = 0 (X[0], X[N]) and j = 8 (X[M])
-    const float2 a0 = va[0], a8 = va[8];
-    float2 tmp[16];
-#pragma unroll
-    for (int j = 1; j < 8; ++j) {
-      tmp[j] = r2c(va[j], va[16 - j], 2u * 1024u * j);
-      tmp[16 - j] = r2c(va[16 - j], va[j], 2u * 1024u * (16 - j));
-    }
-#pragma unroll
-    for (int j = 1; j < 16; ++j) if (j != 8) va[j] = tmp[j];
+    // column 0: pairs j <-> 16-j; self pairs j = 0 (X[0], X[N]) and j = 8 (X[M])
+    const float2 a0 = va[0];
+    static_for<1, 8>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      const float2 P = va[j], Q = va[16 - j];
+      va[j] = r2c(P, Q, w32mul<j>(make_float2(1.f, 0.f)));
+      va[16 - j] = r2c(Q, P, w32mul<16 - j>(make_float2(1.f, 0.f)));
+    });
+    va[8] = r2c(va[8], va[8], w32mul<8>(make_float2(1.f, 0.f)));
     va[0] = make_float2(a0.x + a0.y, 0.f);
     xn = make_float2(a0.x - a0.y, 0.f);
-    va[8] = r2c(a8, a8, 2u * 1024u * 8);
-    // column 512: pairs j <-> 15-j
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    // column 512: bins 1024 + 2048 j, pairs j <-> 15-j ; W_L^1024 = W_64^1
+    const float2 w1 = w64mul<1>(make_float2(1.f, 0.f));
+    static_for<0, 8>([&](auto J) {
+      constexpr int j = decltype(J)::value;
       const float2 P = vb[j], Q = vb[15 - j];
-      vb[j] = r2c(P, Q, 2u * (512u + 1024u * j));
-      vb[15 - j] = r2c(Q, P, 2u * (512u + 1024u * (15 - j)));
-    }
+      vb[j] = r2c(P, Q, w32mul<j>(w1));
+      vb[15 - j] = r2c(Q, P, w32mul<15 - j>(w1));
+    });
   }
-  // bin of register entry: va[j] -> 2 (ka + 1024 j) + r, vb[j] -> 2 (kb + 1024 j) + r
 #define BIN_A(j) (2u * (ka + 1024u * (j)) + r)
 #define BIN_B(j) (2u * (kb + 1024u * (j)) + r)
 
@@ -285,22 +313,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   if (kdrop == 0) mode = kModeKeepAll;
   else if (kdrop >= kBins) mode = kModeDropAll;
   float band_lo = 0.f, band_hi = INFINITY;
+  uint32_t* sub = subhist(sh) + 2048u * ((tid >> 5) & 3u);
   if (mode == kModeList) {
     // pass 1: proxy bits [30:20]
+    __syncthreads();                              // pass-3 reads of buf are done
+    zero_subhist(sh);
+    __syncthreads();
     uint32_t nz = 0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const float pa = proxy_key(va[j].x, va[j].y), pb = proxy_key(vb[j].x, vb[j].y);
-      nz |= __float_as_uint(pa) | __float_as_uint(pb);
-      hist_add(sh.hist, __float_as_uint(pa) >> 20, true);
-      hist_add(sh.hist, __float_as_uint(pb) >> 20, true);
+      const uint32_t pa = __float_as_uint(proxy_key(va[j].x, va[j].y));
+      const uint32_t pb = __float_as_uint(proxy_key(vb[j].x, vb[j].y));
+      nz |= pa | pb;
+      atomicAdd(&sub[pa >> 20], 1u);
+      atomicAdd(&sub[pb >> 20], 1u);
     }
-    {
-      const float pn = proxy_key(xn.x, xn.y);
-      nz |= __float_as_uint(pn);
-      hist_add(sh.hist, __float_as_uint(pn) >> 20, special);
+    if (special) {
+      const uint32_t pn = __float_as_uint(proxy_key(xn.x, xn.y));
+      nz |= pn;
+      atomicAdd(&sub[pn >> 20], 1u);
     }
     if (__any_sync(0xffffffffu, nz != 0) && (tid & 31) == 0) atomicOr(&sh.anynz, 1u);
+    __syncthreads();
+    merge_subhist(sh);
     cluster.sync();
     const bool anynz = (sh.anynz | shp.anynz) != 0;
     uint32_t b1, below1;
@@ -309,20 +344,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     if (!anynz) {
       mode = kModeDropAll;                        // every coefficient is exactly zero: all codes 0
     } else {
-      for (uint32_t b = tid; b < 2048; b += kThreads) sh.hist[b] = 0;
+      zero_subhist(sh);
       __syncthreads();
       // pass 2: proxy bits [19:9] inside bucket b1
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const uint32_t pa = __float_as_uint(proxy_key(va[j].x, va[j].y));
         const uint32_t pb = __float_as_uint(proxy_key(vb[j].x, vb[j].y));
-        hist_add(sh.hist, (pa >> 9) & 0x7FFu, (pa >> 20) == b1);
-        hist_add(sh.hist, (pb >> 9) & 0x7FFu, (pb >> 20) == b1);
+        if ((pa >> 20) == b1) atomicAdd(&sub[(pa >> 9) & 0x7FFu], 1u);
+        if ((pb >> 20) == b1) atomicAdd(&sub[(pb >> 9) & 0x7FFu], 1u);
       }
-      {
+      if (special) {
         const uint32_t pn = __float_as_uint(proxy_key(xn.x, xn.y));
-        hist_add(sh.hist, (pn >> 9) & 0x7FFu, special && (pn >> 20) == b1);
+        if ((pn >> 20) == b1) atomicAdd(&sub[(pn >> 9) & 0x7FFu], 1u);
       }
+      __syncthreads();
+      merge_subhist(sh);
       cluster.sync();
       uint32_t b2, below2;
       merged_bucket(sh, shp.hist, kdrop - 1 - below1, b2, below2);
@@ -336,12 +373,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         band_hi = hi_f * (1.0f + 0x1p-16f);
         // collect undecided bins into CTA 0's list; count the certainly dropped
         uint32_t below_l = 0;
-        auto collect = [&](float2 x, uint32_t bin, bool act) {
-          if (!act) return;
+        auto collect = [&](float2 x, uint32_t bin) {
           const float p = proxy_key(x.x, x.y);
-          if (p < band_lo) {
-            ++below_l;
-          } else if (p < band_hi) {
+          below_l += (p < band_lo) ? 1u : 0u;
+          if (p >= band_lo && p < band_hi) {
             const uint32_t s = atomicAdd(&sh0.ccount, 1u);
             if (s < (uint32_t)kCand) {
               sh0.cidx[s] = bin;
@@ -351,29 +386,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         };
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          collect(va[j], BIN_A(j), true);
-          collect(vb[j], BIN_B(j), true);
+          collect(va[j], BIN_A(j));
+          collect(vb[j], BIN_B(j));
         }
-        collect(xn, kN, special);
+        if (special) collect(xn, kN);
         const uint32_t bl = block_sum<kThreads>(below_l, sh.scan);
         if (tid == 0) sh.below = bl;
       }
       cluster.sync();
       // CTA 0 resolves the undecided bins exactly
       if (r == 0) {
-        __shared__ int dec;
         if (tid == 0) {
           int md = mode;
           const uint32_t m = sh.ccount;
           const uint32_t below = sh.below + shp.below;
-          if (md == kModeList) {
-            if (m > (uint32_t)kCand || below > kdrop || below + m < kdrop) md = kModeFallback;
-          }
+          if (md == kModeList && (m > (uint32_t)kCand || below > kdrop || below + m < kdrop)) md = kModeFallback;
           sh.need = kdrop - below;
-          dec = md;
+          sh.mode = md;
         }
         __syncthreads();
-        mode = dec;
+        mode = sh.mode;
         if (mode == kModeList) {
           const uint32_t m = sh.ccount, need = sh.need;
           uint32_t M2 = 1;
@@ -413,7 +445,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             }
           }
         }
-        if (tid == 0) sh.mode = mode;
       }
       cluster.sync();
       mode = sh0.mode;
@@ -434,116 +465,126 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   }
   if (r == 0 && tid == 0) a.fb[chunk] = 0u;
 
-  // ---- 5. codes for every register bin
+  // ---- 5. codes -> two bin-ordered halves: CTA 0 holds bins [0, 16384),
+  //         CTA 1 holds [16384, 32768]; each zero-fills its half first.
+  __syncthreads();                              // buf (sub-histograms) no longer read
+  {
+    uint4* z = reinterpret_cast<uint4*>(sh.buf);
+    for (uint32_t e = tid; e < (kPadded + 64) / 2; e += kThreads) z[e] = make_uint4(0, 0, 0, 0);
+  }
+  cluster.sync();
   const uint32_t mcount = (mode == kModeList) ? sh0.ccount : 0u;
-  auto dropped = [&](float2 x, uint32_t bin) -> bool {
-    if (mode == kModeKeepAll) return false;
-    if (mode == kModeDropAll) return true;
-    const float p = proxy_key(x.x, x.y);
-    if (p < band_lo) return true;
-    if (p >= band_hi) return false;
-    uint32_t lo = 0, hi = mcount;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if ((sh0.cidx[mid] & 0x7FFFFFFFu) < bin) lo = mid + 1; else hi = mid;
+  uint32_t* arr_own = reinterpret_cast<uint32_t*>(sh.buf);
+  uint32_t* arr_peer = reinterpret_cast<uint32_t*>(shp.buf);
+  auto emit_pair = [&](float2 x, uint32_t bin) {
+    bool drop;
+    if (mode == kModeKeepAll) drop = false;
+    else if (mode == kModeDropAll) drop = true;
+    else {
+      const float p = proxy_key(x.x, x.y);
+      drop = p < band_lo;
+      if (p >= band_lo && p < band_hi) {
+        uint32_t lo = 0, hi = mcount;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if ((sh0.cidx[mid] & 0x7FFFFFFFu) < bin) lo = mid + 1; else hi = mid;
+        }
+        drop = lo < mcount && (sh0.cidx[lo] & 0x7FFFFFFFu) == bin && (sh0.cidx[lo] & 0x80000000u);
+      }
     }
-    return lo < mcount && (sh0.cidx[lo] & 0x7FFFFFFFu) == bin && (sh0.cidx[lo] & 0x80000000u);
+    const uint32_t pc = drop ? 0u : (enc16(q, x.x) | (enc16(q, x.y) << 16));
+    if (pc) {
+      const uint32_t d = bin >= kHalfBins ? 1u : 0u;
+      uint32_t* dst = (d == r) ? arr_own : arr_peer;
+      dst[pad(bin - d * kHalfBins)] = pc;
+    }
   };
-  auto pair_code = [&](float2 x, uint32_t bin) -> uint32_t {
-    if (dropped(x, bin)) return 0u;
-    return encode_code(a.q, x.x) | (encode_code(a.q, x.y) << 16);
-  };
-
-  // ---- 6. bin-ordered code array in CTA 0's shared memory (its FFT buffer)
-  uint32_t* arr = reinterpret_cast<uint32_t*>(sh.buf);       // CTA 0 only
-  uint32_t* arr0 = reinterpret_cast<uint32_t*>(sh0.buf);
-  if (r == 0) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t ba = BIN_A(j), bb = BIN_B(j);
-      arr[pad(ba)] = pair_code(va[j], ba);
-      arr[pad(ba + 1)] = 0u;        // odd neighbour, filled by CTA 1 if non-zero
-      arr[pad(bb)] = pair_code(vb[j], bb);
-      arr[pad(bb + 1)] = 0u;
-    }
-    if (special) arr[pad(kN)] = pair_code(xn, kN);
+  for (int j = 0; j < 16; ++j) {
+    emit_pair(va[j], BIN_A(j));
+    emit_pair(vb[j], BIN_B(j));
   }
+  if (special) emit_pair(xn, kN);
   cluster.sync();
-  if (r == 1) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t ca = pair_code(va[j], BIN_A(j));
-      const uint32_t cb = pair_code(vb[j], BIN_B(j));
-      if (ca) arr0[pad(BIN_A(j))] = ca;
-      if (cb) arr0[pad(BIN_B(j))] = cb;
-    }
-  }
-  cluster.sync();
-  if (r == 1) return;
 #undef BIN_A
 #undef BIN_B
 
-  // ---- 7. CTA 0 packs: thread t owns bins [64t, 64t+64) (+ bin N for t = 511)
-  const int N = a.q.n_bits;
-  const uint32_t b0 = 64u * tid;
-  const uint32_t nb = (tid == kThreads - 1) ? 65u : 64u;
-  uint32_t words[5] = {0, 0, 0, 0, 0};
-  for (uint32_t j = 0; j < nb; ++j) {
-    const uint32_t pc = arr[pad(b0 + j)];
-    const uint32_t bits = ((pc & 0xFFFFu) ? 1u : 0u) | ((pc >> 16) ? 2u : 0u);
-    words[j >> 4] |= bits << (2 * (j & 15));
-  }
+  // ---- 6. pack: thread t of CTA d owns bins d*16384 + [32t, 32t+32) (+ bin N)
+  const int N = q.n_bits;
+  const uint32_t nb = (r == 1 && tid == kThreads - 1) ? 33u : 32u;
+  uint32_t w0 = 0, w1 = 0, w2 = 0;
   uint32_t cnt = 0;
-  const uint32_t nw = (nb + 15) / 16;
+  {
+    const uint32_t* src = arr_own + pad(32u * tid);    // 32 entries + pad: pad(32t + j) = pad(32t) + j
 #pragma unroll
-  for (int w = 0; w < 5; ++w) cnt += __popc(words[w]);
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t pc = src[j];
+      const uint32_t bits = ((pc & 0xFFFFu) ? 1u : 0u) | ((pc >> 16) ? 2u : 0u);
+      if (j < 16) w0 |= bits << (2 * j);
+      else w1 |= bits << (2 * (j - 16));
+    }
+    if (nb == 33) {
+      const uint32_t pc = arr_own[pad(32u * tid + 32u)];
+      w2 = ((pc & 0xFFFFu) ? 1u : 0u) | ((pc >> 16) ? 2u : 0u);
+    }
+    cnt = __popc(w0) + __popc(w1) + __popc(w2);
+  }
   uint32_t* seg = reinterpret_cast<uint32_t*>(a.message + ci.seg_off);
   uint32_t* bm = seg + kSegHeader / 4;
-  for (uint32_t w = 0; w < nw; ++w) bm[4 * tid + w] = ballot_to_wire(words[w]);
-  if (tid == kThreads - 1) {
-    const uint32_t pad_words = (ci.code_off - kSegHeader) / 4;
-    for (uint32_t w = kBmWords; w < pad_words; ++w) bm[w] = 0u;
+  {
+    const uint32_t wb = r * (kHalfBins / 16) + 2u * tid;
+    bm[wb] = ballot_to_wire(w0);
+    bm[wb + 1] = ballot_to_wire(w1);
+    if (nb == 33) {
+      bm[wb + 2] = ballot_to_wire(w2);
+      const uint32_t pad_words = (ci.code_off - kSegHeader) / 4;
+      for (uint32_t w = kBmWords; w < pad_words; ++w) bm[w] = 0u;
+    }
   }
   uint32_t total;
-  const uint32_t base = block_exclusive_scan<kThreads>(cnt, sh.scan, total);
+  uint32_t base = block_exclusive_scan<kThreads>(cnt, sh.scan, total);
+  if (tid == 0) sh.total = total;
+  cluster.sync();
+  if (r == 1) base += sh0.total;
   // emit this thread's codes: bits [base*N, (base+cnt)*N) of the stream
-  uint64_t bitpos = (uint64_t)base * N;
+  const uint64_t bitpos = (uint64_t)base * N;
   uint32_t wcur = (uint32_t)(bitpos >> 5);
   uint32_t fill = (uint32_t)(bitpos & 31u);
-  const bool shared_head = fill != 0;
-  bool first = true;
+  bool shared_word = fill != 0;            // the current word is shared with the previous thread
   uint64_t acc = 0;
   bool overflow = false;
-  auto emit = [&](uint32_t word, bool partial) {
+  auto put = [&](uint32_t word, bool partial) {
     if (wcur >= ci.code_cap) { overflow = true; return; }
-    if (partial || (first && shared_head)) atomicOr(&codes_g[wcur], word);
+    if (partial || shared_word) atomicOr(&codes_g[wcur], word);
     else codes_g[wcur] = word;
   };
-  for (uint32_t w = 0; w < nw; ++w) {
-    uint32_t bits = words[w];
-    while (bits) {
-      const uint32_t pos = __ffs(bits) - 1;
-      bits &= bits - 1;
-      const uint32_t bin = b0 + 16 * w + (pos >> 1);
-      const uint32_t pc = arr[pad(bin)];
+  auto emit_word_bits = [&](uint32_t word, uint32_t jbase) {
+    while (word) {
+      const uint32_t pos = __ffs(word) - 1;
+      word &= word - 1;
+      const uint32_t pc = arr_own[pad(32u * tid + jbase + (pos >> 1))];
       const uint32_t code = (pos & 1) ? (pc >> 16) : (pc & 0xFFFFu);
       acc |= (uint64_t)code << fill;
       fill += N;
       if (fill >= 32) {
-        emit((uint32_t)acc, false);
-        first = false;
+        put((uint32_t)acc, false);
+        shared_word = false;
         acc >>= 32;
         fill -= 32;
         ++wcur;
       }
     }
-  }
-  if (fill > 0 && cnt > 0) emit((uint32_t)acc, true);
-  if (tid == 0) {
-    seg[0] = total;
+  };
+  emit_word_bits(w0, 0);
+  emit_word_bits(w1, 16);
+  emit_word_bits(w2, 32);
+  if (fill > 0 && cnt > 0) put((uint32_t)acc, true);
+  if (r == 1 && tid == 0) {
+    seg[0] = sh0.total + total;
     seg[1] = 0; seg[2] = 0; seg[3] = 0;
   }
   if (overflow) atomicOr(a.flags, FGC_FLAG_CAPACITY);
+  cluster.sync();          // CTA 1 read CTA 0's total; keep both resident until done
 }
 
 // ------------------------------------------------------------------ decode
@@ -559,12 +600,14 @@ struct DecodeArgs {
   float* out;
   const float2* thi;
   const float2* tlo;
+  const float2* t1024;
   const float2* spectrum;     // dense-spectrum mode (debug hook), else null
 };
 
 struct __align__(16) DecodeShared {
   float2 y[kPadded + 64];
   float2 thi[256], tlo[256];
+  float2 t1024[1024];
   uint32_t bm[kBmWords + 3];
   uint32_t pref[kBmWords + 3];
   uint32_t scan[40];
@@ -605,14 +648,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
     sh.thi[tid] = a.thi[tid];
     sh.tlo[tid] = a.tlo[tid];
   }
-  for (uint32_t e = tid; e < kPadded + 64; e += kThreads) sh.y[e] = make_float2(0.f, 0.f);
+  sh.t1024[tid] = a.t1024[tid];
+  sh.t1024[tid + 512] = a.t1024[tid + 512];
+  {
+    float4* z = reinterpret_cast<float4*>(sh.y);
+    for (uint32_t e = tid; e < (kPadded + 64) / 2; e += kThreads) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   __syncthreads();
 
   if (a.spectrum) {
     // dense spectrum input: four quarters, one bin per thread per step
     const float2* X = a.spectrum + ci.bin_off;
-    for (uint32_t q = 0; q < 4; ++q) {
-      const uint32_t lo = q * (kN / 4), hi = (q == 3) ? kBins : (q + 1) * (kN / 4);
+    for (uint32_t qq = 0; qq < 4; ++qq) {
+      const uint32_t lo = qq * (kN / 4), hi = (qq == 3) ? kBins : (qq + 1) * (kN / 4);
       for (uint32_t b = lo + tid; b < hi; b += kThreads) {
         float2 x = X[b];
         if (b == 0 || b == kN) x.y = 0.f;
@@ -633,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
       for (uint32_t k = 0; k < 5; ++k) {
         loc[k] = 0;
         if (k < nw) {
-          loc[k] = ballot_to_wire(bmg[w0 + k]);
+          loc[k] = ballot_to_wire(__ldg(bmg + w0 + k));
           local += __popc(loc[k]);
         }
       }
@@ -649,11 +697,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
       }
       __syncthreads();
       const float wt = a.wts.w[w];
-      for (uint32_t q = 0; q < 4; ++q) {
-        const uint32_t nwq = (q == 3 && tid == 0) ? 2u : 1u;
+      for (uint32_t qq = 0; qq < 4; ++qq) {
+        const uint32_t nwq = (qq == 3 && tid == 0) ? 2u : 1u;
         for (uint32_t e = 0; e < nwq; ++e) {
-          const uint32_t word = (e == 0) ? q * 512u + tid : kBmWords - 1;
-          uint32_t sw = sh.bm[word];
+          const uint32_t word = (e == 0) ? qq * 512u + tid : kBmWords - 1;
+          const uint32_t sw0 = sh.bm[word];
+          uint32_t sw = sw0;
           if (!sw) continue;
           const uint32_t pb = sh.pref[word];
           while (sw) {
@@ -661,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
             const uint32_t jb = pos >> 1;
             const uint32_t bits = (sw >> (2 * jb)) & 3u;
             sw &= ~(3u << (2 * jb));
-            uint32_t rank = pb + __popc(sh.bm[word] & ((1u << (2 * jb)) - 1u));
+            uint32_t rank = pb + __popc(sw0 & ((1u << (2 * jb)) - 1u));
             float re = 0.f, im = 0.f;
             if (bits & 1u) { re = decode_code(a.q, read_bits(cw, (uint64_t)rank * N, N)); ++rank; }
             if (bits & 2u) im = decode_code(a.q, read_bits(cw, (uint64_t)rank * N, N));
@@ -680,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = sh.y[pad(tid + 512u * j)];
   __syncthreads();
-  fft_pass12<true>(v, sh.y, sh.thi, sh.tlo);
+  fft_pass12<true>(v, sh.y, sh.t1024);
   __syncthreads();
   const float scale = 1.0f / (float)kN;
   float* out = a.out + ci.in_off;
@@ -710,11 +759,12 @@ fgc_status fused_tables_init(FusedTables** t, cudaStream_t s) {
   FusedTables* ft = new FusedTables();
   cudaError_t e = cudaMalloc(&ft->thi, 256 * sizeof(float2));
   if (e == cudaSuccess) e = cudaMalloc(&ft->tlo, 256 * sizeof(float2));
+  if (e == cudaSuccess) e = cudaMalloc(&ft->t1024, 1024 * sizeof(float2));
   if (e != cudaSuccess) {
     fused_tables_free(ft);
     return cuda_check(e, "cudaMalloc");
   }
-  k_init_tables<<<1, 256, 0, s>>>(ft->thi, ft->tlo);
+  k_init_tables<<<1, 1024, 0, s>>>(ft->thi, ft->tlo, ft->t1024);
   FGC_LAUNCHED(1);
   static bool attrs = false;
   if (!attrs) {
@@ -733,6 +783,7 @@ void fused_tables_free(FusedTables* t) {
   if (!t) return;
   cudaFree(t->thi);
   cudaFree(t->tlo);
+  cudaFree(t->t1024);
   delete t;
 }
 
@@ -741,7 +792,7 @@ static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_
                                        const QuantParams& q, uint8_t* message, uint32_t* flags, uint32_t* fb,
                                        float2* fb_spec, float2* dbg, cudaStream_t s) {
   if (!count) return FGC_OK;
-  CompressArgs a{d_chunks, first, grad, half_pass, q, message, flags, t->thi, t->tlo, fb, fb_spec, dbg};
+  CompressArgs a{d_chunks, first, grad, half_pass, q, message, flags, t->thi, t->tlo, t->t1024, fb, fb_spec, dbg};
   const size_t smem = sizeof(CompressShared);
   const dim3 grid(2 * count), block(kThreads);
   if (dbg) {
@@ -780,7 +831,7 @@ fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, 
                                const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
                                const QuantParams& q, float* out, cudaStream_t s) {
   if (!count) return FGC_OK;
-  DecodeArgs a{d_chunks, first, messages, W, stride, wts, q, out, t->thi, t->tlo, nullptr};
+  DecodeArgs a{d_chunks, first, messages, W, stride, wts, q, out, t->thi, t->tlo, t->t1024, nullptr};
   k_fused_decode<<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
   FGC_LAUNCHED(1);
   return FGC_OK;
@@ -795,6 +846,7 @@ fgc_status launch_fused_inverse(const FusedTables* t, const ChunkInfo* d_chunks,
   a.out = out;
   a.thi = t->thi;
   a.tlo = t->tlo;
+  a.t1024 = t->t1024;
   a.spectrum = spectrum;
   a.W = 0;
   k_fused_decode<<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);

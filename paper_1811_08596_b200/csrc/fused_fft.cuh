@@ -35,6 +35,10 @@ __device__ constexpr float kS32[16] = {0.0f, 0.19509032201612826f, 0.38268343236
                                         0.83146961230254524f, 0.70710678118654752f, 0.55557023301960222f,
                                         0.38268343236508977f, 0.19509032201612826f};
 
+// cos / sin (2 pi m / 64), m = 0..31
+__device__ constexpr float kC64[32] = {1.0f, 0.99518472667219693f, 0.98078528040323043f, 0.95694033573220882f, 0.92387953251128674f, 0.88192126434835505f, 0.83146961230254524f, 0.77301045336273699f, 0.70710678118654757f, 0.63439328416364549f, 0.55557023301960229f, 0.47139673682599781f, 0.38268343236508984f, 0.29028467725446233f, 0.19509032201612833f, 0.09801714032956077f, 6.123233995736766e-17f, -0.098017140329560645f, -0.19509032201612819f, -0.29028467725446216f, -0.38268343236508973f, -0.4713967368259977f, -0.55557023301960196f, -0.63439328416364538f, -0.70710678118654746f, -0.77301045336273699f, -0.83146961230254535f, -0.88192126434835494f, -0.92387953251128674f, -0.95694033573220882f, -0.98078528040323043f, -0.99518472667219682f};
+__device__ constexpr float kS64[32] = {0.0f, 0.098017140329560604f, 0.19509032201612825f, 0.29028467725446233f, 0.38268343236508978f, 0.47139673682599764f, 0.55557023301960218f, 0.63439328416364549f, 0.70710678118654746f, 0.77301045336273699f, 0.83146961230254524f, 0.88192126434835494f, 0.92387953251128674f, 0.95694033573220894f, 0.98078528040323043f, 0.99518472667219682f, 1.0f, 0.99518472667219693f, 0.98078528040323043f, 0.95694033573220894f, 0.92387953251128674f, 0.88192126434835505f, 0.83146961230254546f, 0.7730104533627371f, 0.70710678118654757f, 0.63439328416364549f, 0.55557023301960218f, 0.47139673682599786f, 0.38268343236508989f, 0.29028467725446239f, 0.19509032201612861f, 0.098017140329560826f};
+
 constexpr int bitrev(int x, int bits) {
   int r = 0;
   for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1) << (bits - 1 - i);
@@ -85,6 +89,26 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
   dif_stages<R / 2, R, INV>(v);
 }
 
+// d * W_64^J (forward), J < 32 compile-time.
+template <int J>
+__device__ __forceinline__ float2 w64mul(float2 d) {
+  if constexpr (J == 0) {
+    return d;
+  } else if constexpr (J == 16) {
+    return make_float2(d.y, -d.x);
+  } else {
+    constexpr float c = kC64[J];
+    constexpr float s = -kS64[J];
+    return make_float2(__fmaf_rn(d.x, c, -d.y * s), __fmaf_rn(d.x, s, d.y * c));
+  }
+}
+// d * W_32^J (forward), J < 32 compile-time.
+template <int J>
+__device__ __forceinline__ float2 w32mul(float2 d) {
+  if constexpr (J < 16) return w64mul<2 * J>(d);
+  else return w64mul<2 * J - 32>(make_float2(-d.x, -d.y));
+}
+
 // W_65536^m from the two-level table (m taken mod 65536).
 __device__ __forceinline__ float2 tw(const float2* thi, const float2* tlo, uint32_t m) {
   return cmul(thi[(m >> 8) & 255u], tlo[m & 255u]);
@@ -99,7 +123,7 @@ __device__ __forceinline__ float2 twc(const float2* thi, const float2* tlo, uint
 // x[i + 512 j]; on exit the pass-2 output sits in `buf` (padded layout),
 // ready for pass 3 (caller syncs).
 template <bool INV>
-__device__ __forceinline__ void fft_pass12(float2 (&v)[32], float2* buf, const float2* thi, const float2* tlo) {
+__device__ __forceinline__ void fft_pass12(float2 (&v)[32], float2* buf, const float2* t1024) {
   const uint32_t i = threadIdx.x;
   dft<32, INV>(v);
 #pragma unroll
@@ -109,7 +133,11 @@ __device__ __forceinline__ void fft_pass12(float2 (&v)[32], float2* buf, const f
   for (int j = 0; j < 32; ++j) v[j] = buf[pad(i + 512 * j)];
   const uint32_t k = i & 31u;
 #pragma unroll
-  for (int j = 1; j < 32; ++j) v[j] = cmul(v[j], twc(thi, tlo, 64u * j * k, INV));   // W_1024^{jk}
+  for (int j = 1; j < 32; ++j) {                   // W_1024^{jk}, jk < 1024
+    float2 w = t1024[j * k];
+    if (INV) w.y = -w.y;
+    v[j] = cmul(v[j], w);
+  }
   dft<32, INV>(v);
   const uint32_t base = (i >> 5) * 1024u + k;
   __syncthreads();                      // every pass-2 read is done before the writes

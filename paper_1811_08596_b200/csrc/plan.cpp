@@ -46,6 +46,8 @@ struct fgc_plan {
   float2* d_spec = nullptr;
   uint64_t* d_scratch = nullptr;
   uint32_t* d_fb = nullptr;          // per-chunk fused-kernel fallback flags
+  cudaStream_t side = nullptr;       // generic (tail) classes overlap the fused kernels here
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   FusedTables* fused = nullptr;
   uint32_t fused_first = 0, fused_count = 0;     // chunk range taken by fused kernels
 };
@@ -202,6 +204,12 @@ extern "C" fgc_status fgc_plan_create(const fgc_codec_desc* desc, fgc_plan** out
     return fail(cuda_check(e, "cudaMalloc"));
   if ((e = cudaMemset(p->d_fb, 0, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
     return fail(cuda_check(e, "cudaMemset"));
+  if ((e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(cuda_check(e, "cudaStreamCreate"));
+  if ((e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming)) != cudaSuccess)
+    return fail(cuda_check(e, "cudaEventCreate"));
+  if ((e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming)) != cudaSuccess)
+    return fail(cuda_check(e, "cudaEventCreate"));
   for (RealClass& rc : p->classes) {
     if (rc.fused) {
       fgc_status st = fused_tables_init(&p->fused, s);
@@ -226,6 +234,9 @@ extern "C" void fgc_plan_destroy(fgc_plan* p) {
   cudaFree(p->d_spec);
   cudaFree(p->d_scratch);
   cudaFree(p->d_fb);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
+  if (p->side) cudaStreamDestroy(p->side);
   delete p;
 }
 
@@ -284,6 +295,18 @@ extern "C" fgc_status fgc_compress(fgc_plan* p, const void* grad, int dtype, uin
   if (!p || !grad || !message || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
   FGC_TRY(check_mode(p));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // generic classes (tails) run on the side stream, overlapped with the fused kernel
+  const bool fork = p->fused_count && p->classes.size() > 1;
+  cudaStream_t g = fork ? p->side : s;
+  if (fork) {
+    FGC_CUDA(cudaEventRecord(p->ev_fork, s));
+    FGC_CUDA(cudaStreamWaitEvent(g, p->ev_fork, 0));
+  }
+  FGC_TRY(forward_generic(p, grad, dtype, p->d_spec, flags, g, false));
+  for (RealClass& rc : p->classes) {
+    if (rc.fused) continue;
+    FGC_TRY(launch_select_pack(p->d_chunks, rc.first, rc.count, p->d_spec, 0, p->q, message, nullptr, flags, g));
+  }
   if (p->fused_count) {
     FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, p->fused_first, p->fused_count, grad, dtype,
                                   p->desc.half_pass, p->q, message, flags, p->d_fb, p->d_spec, s));
@@ -291,11 +314,9 @@ extern "C" fgc_status fgc_compress(fgc_plan* p, const void* grad, int dtype, uin
     FGC_TRY(launch_select_pack(p->d_chunks, p->fused_first, p->fused_count, p->d_spec, 0, p->q, message, nullptr,
                                flags, s, p->d_fb));
   }
-  FGC_TRY(forward_generic(p, grad, dtype, p->d_spec, flags, s, false));
-  // generic chunks are the ones outside [fused_first, fused_first + fused_count)
-  for (RealClass& rc : p->classes) {
-    if (rc.fused) continue;
-    FGC_TRY(launch_select_pack(p->d_chunks, rc.first, rc.count, p->d_spec, 0, p->q, message, nullptr, flags, s));
+  if (fork) {
+    FGC_CUDA(cudaEventRecord(p->ev_join, g));
+    FGC_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
   }
   return FGC_OK;
 }
@@ -343,15 +364,26 @@ extern "C" fgc_status fgc_decode_average(fgc_plan* p, const uint8_t* messages, i
   Weights w;
   FGC_TRY(fill_weights(weights, W, w));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (p->fused_count)
-    FGC_TRY(launch_fused_decode(p->fused, p->d_chunks, p->fused_first, p->fused_count, messages, W, stride, w, p->q,
-                                out, s));
+  const bool fork = p->fused_count && p->classes.size() > 1;
+  cudaStream_t g = fork ? p->side : s;
+  if (fork) {
+    FGC_CUDA(cudaEventRecord(p->ev_fork, s));
+    FGC_CUDA(cudaStreamWaitEvent(g, p->ev_fork, 0));
+  }
   for (RealClass& rc : p->classes) {
     if (rc.fused) continue;
     FGC_TRY(launch_decode_accumulate(p->d_chunks, rc.first, rc.count, messages, W, stride, w, p->q, p->d_spec,
-                                     p->max_slots, s));
+                                     p->max_slots, g));
   }
-  return inverse_generic(p, p->d_spec, out, s);
+  FGC_TRY(inverse_generic(p, p->d_spec, out, g));
+  if (p->fused_count)
+    FGC_TRY(launch_fused_decode(p->fused, p->d_chunks, p->fused_first, p->fused_count, messages, W, stride, w, p->q,
+                                out, s));
+  if (fork) {
+    FGC_CUDA(cudaEventRecord(p->ev_join, g));
+    FGC_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
+  }
+  return FGC_OK;
 }
 
 extern "C" fgc_status fgc_decode_spectrum(fgc_plan* p, const uint8_t* messages, int W, uint64_t stride,
