@@ -50,6 +50,9 @@ def stale(force: bool) -> bool:
     if force or not OUT.exists():
         return True
     t = OUT.stat().st_mtime
+    flags_file = PKG / "libfgc_b200.flags"
+    if not flags_file.exists() or flags_file.read_text() != os.environ.get("FGC_NVCC_FLAGS", ""):
+        return True
     return any(p.stat().st_mtime > t for p in sources() + headers() + [Path(__file__)])
 
 
@@ -61,6 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     cc = nvcc()
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I", str(inc),
               "-I", str(ROOT / "include"), "--expt-relaxed-constexpr"]
+    common += os.environ.get("FGC_NVCC_FLAGS", "").split()
 
     def compile_one(src: Path):
         obj = OBJ / (src.name + ".o")
@@ -83,6 +87,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     tmp.replace(OUT)
+    (PKG / "libfgc_b200.flags").write_text(os.environ.get("FGC_NVCC_FLAGS", ""))
     return OUT
 
 

@@ -126,7 +126,7 @@ class Plan:
 
 
 _PLANS: "OrderedDict[tuple, Plan]" = OrderedDict()
-_PLAN_CACHE = 16
+_PLAN_CACHE = int(__import__("os").environ.get("FGC_PLAN_CACHE", "16"))
 
 
 def get_plan(n: int, chunk: int, theta: float, mode: str, half: bool, quant: QuantizerConfig | None,

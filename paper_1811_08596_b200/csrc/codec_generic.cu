@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
     const uint32_t r0 = rank_base + wbase + pre;
     // stage the codes (LSB-first N-bit fields, bit 0 of stage[0] = word `origin`)
     const uint64_t obit = (uint64_t)origin * 32u;
+    FGC_CHECK((uint64_t)(r0 + 2) * N - obit < 32ull * stage_words);
     if (cre) {
       const uint64_t lb = (uint64_t)r0 * N - obit;
       const uint32_t o = (uint32_t)(lb & 31u);

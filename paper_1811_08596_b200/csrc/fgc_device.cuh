@@ -12,6 +12,23 @@
 
 #include "fgc_types.h"
 
+// Debug-only bounds checks (build with FGC_NVCC_FLAGS=-DFGC_BOUNDS).
+#ifdef FGC_BOUNDS
+#include <cstdio>
+#define FGC_CHECK(cond)                                                                            \
+  do {                                                                                             \
+    if (!(cond)) {                                                                                 \
+      printf("FGC_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x,   \
+             threadIdx.x, #cond);                                                                  \
+      __trap();                                                                                    \
+    }                                                                                              \
+  } while (0)
+#else
+#define FGC_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace fgc {
 
 // ---------------------------------------------------------------- quantizer

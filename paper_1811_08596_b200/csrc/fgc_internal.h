@@ -22,11 +22,13 @@ void count_launch(uint64_t n = 1);
     cudaError_t e_ = (call);                                            \
     if (e_ != cudaSuccess) return ::fgc::cuda_check(e_, #call);         \
   } while (0)
-#define FGC_LAUNCHED(n)                                                 \
-  do {                                                                  \
-    ::fgc::count_launch(n);                                             \
-    cudaError_t e_ = cudaGetLastError();                                \
-    if (e_ != cudaSuccess) return ::fgc::cuda_check(e_, "kernel launch"); \
+#define FGC_STR2(x) #x
+#define FGC_STR(x) FGC_STR2(x)
+#define FGC_LAUNCHED(n)                                                                       \
+  do {                                                                                        \
+    ::fgc::count_launch(n);                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                      \
+    if (e_ != cudaSuccess) return ::fgc::cuda_check(e_, "kernel launch " __FILE__ ":" FGC_STR(__LINE__)); \
   } while (0)
 #define FGC_TRY(expr)                                                   \
   do {                                                                  \

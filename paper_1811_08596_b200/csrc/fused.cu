@@ -52,6 +52,8 @@ struct FusedTables {
   float2* t1024 = nullptr;   // W_1024^m, m < 1024
 };
 
+__device__ uint32_t g_fused_dbg = 0;   // fault-bisection knobs (0 in production)
+
 namespace {
 
 using namespace ff;
@@ -60,6 +62,9 @@ constexpr int kCand = 1024;
 constexpr uint32_t kBins = kN + 1;                     // 32769
 constexpr uint32_t kBmWords = (2 * kBins + 31) / 32;  // 2049
 constexpr uint32_t kHalfBins = kN / 2;                 // 16384: pack split point
+constexpr uint32_t kStageOff = 16900;                  // u32 offset of the code-stream staging in buf
+static_assert(kStageOff > (kHalfBins + kHalfBins / 32) &&
+              kStageOff + (32 + (kHalfBins + 1) * 32 + 31) / 32 <= 2 * (kPadded + 64), "staging fits in buf");
 
 template <int B, int E, class F>
 __device__ __forceinline__ void static_for(F&& f) {
@@ -210,6 +215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   CompressShared& sh0 = *cluster.map_shared_rank(&sh, 0);
   CompressShared& shp = *cluster.map_shared_rank(&sh, r ^ 1);
   const QuantParams q = a.q;
+  const uint32_t dbg = g_fused_dbg;
 
   if (tid < 256) {
     sh.thi[tid] = a.thi[tid];
@@ -218,10 +224,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   sh.t1024[tid] = a.t1024[tid];
   sh.t1024[tid + 512] = a.t1024[tid + 512];
   if (tid == 0) { sh.ccount = 0; sh.below = 0; sh.anynz = 0; }
-  uint32_t* codes_g = reinterpret_cast<uint32_t*>(a.message + ci.seg_off + ci.code_off);
-  const uint32_t cap_padded = (ci.code_cap + 3u) & ~3u;
-  if (!DEBUG && r == 0)
-    for (uint32_t w = tid; w < cap_padded; w += kThreads) codes_g[w] = 0;   // red.or targets
+  uint32_t* codes_g = DEBUG ? nullptr : reinterpret_cast<uint32_t*>(a.message + ci.seg_off + ci.code_off);
   __syncthreads();
 
   // ---- 1. load + decimation-in-frequency split (pass-1 input layout)
@@ -324,15 +327,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     for (int j = 0; j < 16; ++j) {
       const uint32_t pa = __float_as_uint(proxy_key(va[j].x, va[j].y));
       const uint32_t pb = __float_as_uint(proxy_key(vb[j].x, vb[j].y));
-      nz |= pa | pb;
+      nz |= __float_as_uint(va[j].x) | __float_as_uint(va[j].y) | __float_as_uint(vb[j].x) |
+            __float_as_uint(vb[j].y);
+      FGC_CHECK((pa >> 20) < 2048u && (pb >> 20) < 2048u);
       atomicAdd(&sub[pa >> 20], 1u);
       atomicAdd(&sub[pb >> 20], 1u);
     }
     if (special) {
       const uint32_t pn = __float_as_uint(proxy_key(xn.x, xn.y));
-      nz |= pn;
+      nz |= __float_as_uint(xn.x) | __float_as_uint(xn.y);
       atomicAdd(&sub[pn >> 20], 1u);
     }
+    nz &= 0x7FFFFFFFu;                            // -0.0 is zero
     if (__any_sync(0xffffffffu, nz != 0) && (tid & 31) == 0) atomicOr(&sh.anynz, 1u);
     __syncthreads();
     merge_subhist(sh);
@@ -483,7 +489,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     else {
       const float p = proxy_key(x.x, x.y);
       drop = p < band_lo;
-      if (p >= band_lo && p < band_hi) {
+      if (p >= band_lo && p < band_hi && !(dbg & 4u)) {
         uint32_t lo = 0, hi = mcount;
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
@@ -496,7 +502,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     if (pc) {
       const uint32_t d = bin >= kHalfBins ? 1u : 0u;
       uint32_t* dst = (d == r) ? arr_own : arr_peer;
-      dst[pad(bin - d * kHalfBins)] = pc;
+      FGC_CHECK(bin <= kN && pad(bin - d * kHalfBins) < 2u * (kPadded + 64));
+      if (d == r || !(dbg & 2u)) dst[pad(bin - d * kHalfBins)] = pc;
     }
   };
 #pragma unroll
@@ -508,6 +515,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   cluster.sync();
 #undef BIN_A
 #undef BIN_B
+  if (dbg & 8u) {
+    cluster.sync();
+    return;
+  }
 
   // ---- 6. pack: thread t of CTA d owns bins d*16384 + [32t, 32t+32) (+ bin N)
   const int N = q.n_bits;
@@ -542,49 +553,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     }
   }
   uint32_t total;
-  uint32_t base = block_exclusive_scan<kThreads>(cnt, sh.scan, total);
+  const uint32_t base = block_exclusive_scan<kThreads>(cnt, sh.scan, total);
   if (tid == 0) sh.total = total;
   cluster.sync();
-  if (r == 1) base += sh0.total;
-  // emit this thread's codes: bits [base*N, (base+cnt)*N) of the stream
-  const uint64_t bitpos = (uint64_t)base * N;
-  uint32_t wcur = (uint32_t)(bitpos >> 5);
-  uint32_t fill = (uint32_t)(bitpos & 31u);
-  bool shared_word = fill != 0;            // the current word is shared with the previous thread
-  uint64_t acc = 0;
-  bool overflow = false;
-  auto put = [&](uint32_t word, bool partial) {
-    if (wcur >= ci.code_cap) { overflow = true; return; }
-    if (partial || shared_word) atomicOr(&codes_g[wcur], word);
-    else codes_g[wcur] = word;
-  };
-  auto emit_word_bits = [&](uint32_t word, uint32_t jbase) {
-    while (word) {
-      const uint32_t pos = __ffs(word) - 1;
-      word &= word - 1;
-      const uint32_t pc = arr_own[pad(32u * tid + jbase + (pos >> 1))];
-      const uint32_t code = (pos & 1) ? (pc >> 16) : (pc & 0xFFFFu);
-      acc |= (uint64_t)code << fill;
-      fill += N;
-      if (fill >= 32) {
-        put((uint32_t)acc, false);
-        shared_word = false;
-        acc >>= 32;
-        fill -= 32;
-        ++wcur;
+  const uint32_t t0 = sh0.total;                         // codes in CTA 0's half
+  const uint32_t all = t0 + shp.total * (1u - r) + total * r;   // t0 + t1
+  // This CTA's half of the stream starts at global bit S = (r ? t0 : 0) * N.
+  // It is assembled in a shared staging area (after the code array in buf):
+  // local word k <-> global word (S >> 5) + k; bit offset o = S & 31.
+  const uint64_t S = (uint64_t)(r ? t0 : 0u) * N;
+  const uint32_t wstart = (uint32_t)(S >> 5), o = (uint32_t)(S & 31u);
+  const uint32_t nwords = (uint32_t)((o + (uint64_t)total * N + 31) / 32);
+  uint32_t* stg = arr_own + kStageOff;
+  for (uint32_t k = tid; k < nwords; k += kThreads) stg[k] = 0u;
+  __syncthreads();
+  {
+    uint64_t lbit = o + (uint64_t)base * N;              // local bit position of my first code
+    auto emit_word_bits = [&](uint32_t word, uint32_t jbase) {
+      while (word) {
+        const uint32_t pos = __ffs(word) - 1;
+        word &= word - 1;
+        const uint32_t pc = arr_own[pad(32u * tid + jbase + (pos >> 1))];
+        const uint32_t code = (pos & 1) ? (pc >> 16) : (pc & 0xFFFFu);
+        const uint32_t wi = (uint32_t)(lbit >> 5), sh_ = (uint32_t)(lbit & 31u);
+        atomicOr(&stg[wi], code << sh_);
+        if (sh_ + N > 32u) atomicOr(&stg[wi + 1], code >> (32u - sh_));
+        lbit += N;
       }
-    }
-  };
-  emit_word_bits(w0, 0);
-  emit_word_bits(w1, 16);
-  emit_word_bits(w2, 32);
-  if (fill > 0 && cnt > 0) put((uint32_t)acc, true);
-  if (r == 1 && tid == 0) {
-    seg[0] = sh0.total + total;
-    seg[1] = 0; seg[2] = 0; seg[3] = 0;
+    };
+    emit_word_bits(w0, 0);
+    emit_word_bits(w1, 16);
+    emit_word_bits(w2, 32);
   }
-  if (overflow) atomicOr(a.flags, FGC_FLAG_CAPACITY);
-  cluster.sync();          // CTA 1 read CTA 0's total; keep both resident until done
+  __syncthreads();
+  cluster.sync();          // both halves staged
+  // CTA 1's first word is shared with CTA 0's last one when t0*N is not word
+  // aligned: CTA 0 folds it in and owns that word.
+  if (r == 0 && tid == 0) {
+    const uint64_t s1 = (uint64_t)t0 * N;
+    if (s1 & 31u) stg[s1 >> 5] |= (reinterpret_cast<const uint32_t*>(shp.buf) + kStageOff)[0];
+  }
+  __syncthreads();
+  // coalesced write-out (CTA 0 owns the shared word); zero the unused capacity
+  const uint32_t first = (r == 1 && o != 0) ? 1u : 0u;
+  const uint32_t used = (uint32_t)(((uint64_t)all * N + 31) / 32);
+  const uint32_t cap_padded = (ci.code_cap + 3u) & ~3u;
+  for (uint32_t k = first + tid; k < nwords; k += kThreads) {
+    if (wstart + k < ci.code_cap) codes_g[wstart + k] = stg[k];
+  }
+  if (r == 1)
+    for (uint32_t w = used + tid; w < cap_padded; w += kThreads) codes_g[w] = 0u;
+  if (r == 1 && tid == 0) {
+    seg[0] = all;
+    seg[1] = 0; seg[2] = 0; seg[3] = 0;
+    if (used > ci.code_cap) atomicOr(a.flags, FGC_FLAG_CAPACITY);
+  }
+  cluster.sync();          // peers finished their DSMEM reads; keep both resident until done
 }
 
 // ------------------------------------------------------------------ decode
@@ -754,6 +778,15 @@ fgc_status set_smem(K kernel, size_t bytes) {
 }  // namespace
 
 bool fused_available() { return true; }
+
+}  // namespace fgc
+
+// Internal fault-bisection hook (not part of the public header).
+extern "C" int fgc_debug_set_fused_knobs(uint32_t knobs) {
+  return cudaMemcpyToSymbol(fgc::g_fused_dbg, &knobs, sizeof(knobs)) == cudaSuccess ? 0 : 1;
+}
+
+namespace fgc {
 
 fgc_status fused_tables_init(FusedTables** t, cudaStream_t s) {
   FusedTables* ft = new FusedTables();
