@@ -121,9 +121,9 @@ template <> struct In<double> {
 // encode_code specialised for N <= 16 (no passthrough branch)
 __device__ __forceinline__ uint32_t enc16(const QuantParams& q, float x) {
   const float a = fabsf(x);
-  const uint32_t op = (__float_as_uint(fminf(a, q.pos_cap)) >> q.shift) - q.pbase + 1u;
-  const uint32_t on = (__float_as_uint(fminf(a, q.neg_cap)) >> q.shift) - q.pbase + 1u;
-  const uint32_t c = (x > 0.0f) ? min(op, q.npos) : q.npos + min(on, q.nneg);
+  const bool pos = x > 0.0f;
+  const uint32_t off = (__float_as_uint(fminf(a, pos ? q.pos_cap : q.neg_cap)) >> q.shift) - q.pbase + 1u;
+  const uint32_t c = pos ? min(off, q.npos) : q.npos + min(off, q.nneg);
   return (a < q.eps) ? 0u : c;
 }
 
@@ -203,7 +203,26 @@ __device__ __forceinline__ void merge_subhist(CompressShared& sh) {
   for (uint32_t b = threadIdx.x; b < 2048; b += kThreads) sh.hist[b] = s[b] + s[2048 + b] + s[4096 + b] + s[6144 + b];
 }
 
-template <class T, bool DEBUG>
+// Rare paths kept out of line so the 32-way unrolled per-bin loops stay small
+// (instruction-cache pressure is the fused kernel's first-order stall).
+__device__ __noinline__ bool inband_dropped(const CompressShared* sh0, uint32_t mcount, uint32_t bin) {
+  uint32_t lo = 0, hi = mcount;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((sh0->cidx[mid] & 0x7FFFFFFFu) < bin) lo = mid + 1; else hi = mid;
+  }
+  return lo < mcount && (sh0->cidx[lo] & 0x7FFFFFFFu) == bin && (sh0->cidx[lo] & 0x80000000u);
+}
+
+__device__ __noinline__ void push_candidate(CompressShared* sh0, uint32_t bin, float re, float im) {
+  const uint32_t s = atomicAdd(&sh0->ccount, 1u);
+  if (s < (uint32_t)kCand) {
+    sh0->cidx[s] = bin;
+    sh0->ckey[s] = (unsigned long long)__double_as_longlong(cabs_key((double)re, (double)im));
+  }
+}
+
+template <class T, bool DEBUG, bool HALF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused_compress(CompressArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CompressShared& sh = *reinterpret_cast<CompressShared*>(smem_raw);
@@ -236,8 +255,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     static_for<0, 32>([&](auto J) {
       constexpr int j = decltype(J)::value;
       const uint32_t n = tid + 512u * j;
-      const float2 z0 = In<T>::get(g, 2ull * n, a.half, bad);
-      const float2 z1 = In<T>::get(g, 2ull * (n + kM), a.half, bad);
+      const float2 z0 = In<T>::get(g, 2ull * n, HALF, bad);
+      const float2 z1 = In<T>::get(g, 2ull * (n + kM), HALF, bad);
       if (r == 0) {
         v[j] = make_float2(z0.x + z1.x, z0.y + z1.y);
       } else {                                              // (z0 - z1) W_N^(tid + 512 j)
@@ -382,13 +401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         auto collect = [&](float2 x, uint32_t bin) {
           const float p = proxy_key(x.x, x.y);
           below_l += (p < band_lo) ? 1u : 0u;
-          if (p >= band_lo && p < band_hi) {
-            const uint32_t s = atomicAdd(&sh0.ccount, 1u);
-            if (s < (uint32_t)kCand) {
-              sh0.cidx[s] = bin;
-              sh0.ckey[s] = (unsigned long long)__double_as_longlong(cabs_key((double)x.x, (double)x.y));
-            }
-          }
+          if (p >= band_lo && p < band_hi) push_candidate(&sh0, bin, x.x, x.y);
         };
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -482,28 +495,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   const uint32_t mcount = (mode == kModeList) ? sh0.ccount : 0u;
   uint32_t* arr_own = reinterpret_cast<uint32_t*>(sh.buf);
   uint32_t* arr_peer = reinterpret_cast<uint32_t*>(shp.buf);
+  // band in the proxy domain; KeepAll / DropAll become degenerate bands
+  float lo_b = band_lo, hi_b = band_hi;
+  if (mode == kModeKeepAll) { lo_b = -1.0f; hi_b = -1.0f; }
+  if (mode == kModeDropAll) { lo_b = INFINITY; hi_b = INFINITY; }
   auto emit_pair = [&](float2 x, uint32_t bin) {
-    bool drop;
-    if (mode == kModeKeepAll) drop = false;
-    else if (mode == kModeDropAll) drop = true;
-    else {
-      const float p = proxy_key(x.x, x.y);
-      drop = p < band_lo;
-      if (p >= band_lo && p < band_hi && !(dbg & 4u)) {
-        uint32_t lo = 0, hi = mcount;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if ((sh0.cidx[mid] & 0x7FFFFFFFu) < bin) lo = mid + 1; else hi = mid;
-        }
-        drop = lo < mcount && (sh0.cidx[lo] & 0x7FFFFFFFu) == bin && (sh0.cidx[lo] & 0x80000000u);
+    const float p = proxy_key(x.x, x.y);
+    bool keep = p >= lo_b;
+    if (keep && p < hi_b) keep = !inband_dropped(&sh0, mcount, bin);
+    if (keep) {
+      const uint32_t pc = enc16(q, x.x) | (enc16(q, x.y) << 16);
+      if (pc) {
+        const uint32_t d = bin >= kHalfBins ? 1u : 0u;
+        uint32_t* dst = (d == r) ? arr_own : arr_peer;
+        FGC_CHECK(bin <= kN && pad(bin - d * kHalfBins) < 2u * (kPadded + 64));
+        dst[pad(bin - d * kHalfBins)] = pc;
       }
-    }
-    const uint32_t pc = drop ? 0u : (enc16(q, x.x) | (enc16(q, x.y) << 16));
-    if (pc) {
-      const uint32_t d = bin >= kHalfBins ? 1u : 0u;
-      uint32_t* dst = (d == r) ? arr_own : arr_peer;
-      FGC_CHECK(bin <= kN && pad(bin - d * kHalfBins) < 2u * (kPadded + 64));
-      if (d == r || !(dbg & 2u)) dst[pad(bin - d * kHalfBins)] = pc;
     }
   };
 #pragma unroll
@@ -638,12 +645,12 @@ struct __align__(16) DecodeShared {
 };
 
 // Add the contributions of bin b's (weighted) value X to Y_r.
-__device__ __forceinline__ void scatter_bin(DecodeShared& sh, uint32_t r, uint32_t b, float2 X) {
-  const float2 wb = tw(sh.thi, sh.tlo, b);                      // W_L^b
+// wb = W_L^b.
+__device__ __forceinline__ void scatter_bin(DecodeShared& sh, uint32_t r, uint32_t b, float2 X, float2 wb) {
   float2 cA = make_float2(0.5f * (1.0f + wb.y), 0.5f * wb.x);   // (1 + i W_L^-b)/2
   float2 cB = make_float2(0.5f * (1.0f - wb.y), 0.5f * wb.x);   // (1 + i W_L^b)/2
   if (r) {
-    const float2 w2 = tw(sh.thi, sh.tlo, 2u * b);               // W_N^b
+    const float2 w2 = cmul(wb, wb);                             // W_N^b = (W_L^b)^2
     cA = cmulc(cA, w2);                                         // * W_N^-b
     cB = cmul(cB, w2);                                          // * W_N^b
   }
@@ -688,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
       for (uint32_t b = lo + tid; b < hi; b += kThreads) {
         float2 x = X[b];
         if (b == 0 || b == kN) x.y = 0.f;
-        scatter_bin(sh, r, b, x);
+        scatter_bin(sh, r, b, x, tw(sh.thi, sh.tlo, b));
       }
       __syncthreads();
     }
@@ -729,6 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
           uint32_t sw = sw0;
           if (!sw) continue;
           const uint32_t pb = sh.pref[word];
+          const float2 wbase = tw(sh.thi, sh.tlo, 16u * word);
           while (sw) {
             const uint32_t pos = __ffs(sw) - 1;          // lowest set slot bit
             const uint32_t jb = pos >> 1;
@@ -740,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
             if (bits & 2u) im = decode_code(a.q, read_bits(cw, (uint64_t)rank * N, N));
             const uint32_t b = word * 16u + jb;
             if (b == 0 || b == kN) im = 0.f;
-            scatter_bin(sh, r, b, make_float2(re * wt, im * wt));
+            scatter_bin(sh, r, b, make_float2(re * wt, im * wt), cmul(wbase, sh.tlo[jb]));   // W_L^(16 word + jb)
           }
         }
         __syncthreads();
@@ -801,10 +809,15 @@ fgc_status fused_tables_init(FusedTables** t, cudaStream_t s) {
   FGC_LAUNCHED(1);
   static bool attrs = false;
   if (!attrs) {
-    FGC_TRY(set_smem(k_fused_compress<float, false>, sizeof(CompressShared)));
-    FGC_TRY(set_smem(k_fused_compress<double, false>, sizeof(CompressShared)));
-    FGC_TRY(set_smem(k_fused_compress<float, true>, sizeof(CompressShared)));
-    FGC_TRY(set_smem(k_fused_compress<double, true>, sizeof(CompressShared)));
+    const size_t cs = sizeof(CompressShared);
+    FGC_TRY(set_smem(k_fused_compress<float, false, false>, cs));
+    FGC_TRY(set_smem(k_fused_compress<double, false, false>, cs));
+    FGC_TRY(set_smem(k_fused_compress<float, true, false>, cs));
+    FGC_TRY(set_smem(k_fused_compress<double, true, false>, cs));
+    FGC_TRY(set_smem(k_fused_compress<float, false, true>, cs));
+    FGC_TRY(set_smem(k_fused_compress<double, false, true>, cs));
+    FGC_TRY(set_smem(k_fused_compress<float, true, true>, cs));
+    FGC_TRY(set_smem(k_fused_compress<double, true, true>, cs));
     FGC_TRY(set_smem(k_fused_decode, sizeof(DecodeShared)));
     attrs = true;
   }
@@ -828,13 +841,16 @@ static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_
   CompressArgs a{d_chunks, first, grad, half_pass, q, message, flags, t->thi, t->tlo, t->t1024, fb, fb_spec, dbg};
   const size_t smem = sizeof(CompressShared);
   const dim3 grid(2 * count), block(kThreads);
+  const bool f64 = dtype == FGC_DTYPE_F64, h = half_pass != 0;
+#define FGC_LAUNCH_FC(T, D, H) k_fused_compress<T, D, H><<<grid, block, smem, s>>>(a)
   if (dbg) {
-    if (dtype == FGC_DTYPE_F64) k_fused_compress<double, true><<<grid, block, smem, s>>>(a);
-    else k_fused_compress<float, true><<<grid, block, smem, s>>>(a);
+    if (f64) { if (h) FGC_LAUNCH_FC(double, true, true); else FGC_LAUNCH_FC(double, true, false); }
+    else { if (h) FGC_LAUNCH_FC(float, true, true); else FGC_LAUNCH_FC(float, true, false); }
   } else {
-    if (dtype == FGC_DTYPE_F64) k_fused_compress<double, false><<<grid, block, smem, s>>>(a);
-    else k_fused_compress<float, false><<<grid, block, smem, s>>>(a);
+    if (f64) { if (h) FGC_LAUNCH_FC(double, false, true); else FGC_LAUNCH_FC(double, false, false); }
+    else { if (h) FGC_LAUNCH_FC(float, false, true); else FGC_LAUNCH_FC(float, false, false); }
   }
+#undef FGC_LAUNCH_FC
   FGC_LAUNCHED(1);
   return FGC_OK;
 }

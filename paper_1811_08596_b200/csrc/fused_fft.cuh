@@ -126,11 +126,13 @@ template <bool INV>
 __device__ __forceinline__ void fft_pass12(float2 (&v)[32], float2* buf, const float2* t1024) {
   const uint32_t i = threadIdx.x;
   dft<32, INV>(v);
+  float2* w1 = buf + 33u * i;                           // pad(32 i + m) = 33 i + m
 #pragma unroll
-  for (int m = 0; m < 32; ++m) buf[pad(32 * i + m)] = v[bitrev(m, 5)];
+  for (int m = 0; m < 32; ++m) w1[m] = v[bitrev(m, 5)];
   __syncthreads();
+  const float2* r2 = buf + i + (i >> 5);                // pad(i + 512 j) = i + i/32 + 528 j
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = buf[pad(i + 512 * j)];
+  for (int j = 0; j < 32; ++j) v[j] = r2[528 * j];
   const uint32_t k = i & 31u;
 #pragma unroll
   for (int j = 1; j < 32; ++j) {                   // W_1024^{jk}, jk < 1024
@@ -139,10 +141,10 @@ __device__ __forceinline__ void fft_pass12(float2 (&v)[32], float2* buf, const f
     v[j] = cmul(v[j], w);
   }
   dft<32, INV>(v);
-  const uint32_t base = (i >> 5) * 1024u + k;
+  float2* w2 = buf + (i >> 5) * 1056u + k;             // pad((i/32)*1024 + k + 32 m) = (i/32)*1056 + k + 33 m
   __syncthreads();                      // every pass-2 read is done before the writes
 #pragma unroll
-  for (int m = 0; m < 32; ++m) buf[pad(base + 32 * m)] = v[bitrev(m, 5)];
+  for (int m = 0; m < 32; ++m) w2[33 * m] = v[bitrev(m, 5)];
 }
 
 // Pass 3 for one column k: reads x[k + 1024 j] (j < 16) from buf, applies
@@ -151,8 +153,9 @@ template <bool INV>
 __device__ __forceinline__ void fft_pass3(uint32_t k, const float2* buf, float2 (&out)[16], const float2* thi,
                                           const float2* tlo) {
   float2 v[16];
+  const float2* r3 = buf + k + (k >> 5);                // pad(k + 1024 j) = k + k/32 + 1056 j
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = buf[pad(k + 1024u * j)];
+  for (int j = 0; j < 16; ++j) v[j] = r3[1056 * j];
 #pragma unroll
   for (int j = 1; j < 16; ++j) v[j] = cmul(v[j], twc(thi, tlo, 4u * j * k, INV));    // W_16384^{jk}
   dft<16, INV>(v);
