@@ -204,8 +204,14 @@ extern "C" fgc_status fgc_plan_create(const fgc_codec_desc* desc, fgc_plan** out
     return fail(cuda_check(e, "cudaMalloc"));
   if ((e = cudaMemset(p->d_fb, 0, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
     return fail(cuda_check(e, "cudaMemset"));
-  if ((e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking)) != cudaSuccess)
-    return fail(cuda_check(e, "cudaStreamCreate"));
+  {
+    // the side stream carries the small tail-chunk kernels: give them priority
+    // so they take SMs as soon as the wide fused kernels release any
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if ((e = cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, greatest)) != cudaSuccess)
+      return fail(cuda_check(e, "cudaStreamCreate"));
+  }
   if ((e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming)) != cudaSuccess)
     return fail(cuda_check(e, "cudaEventCreate"));
   if ((e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming)) != cudaSuccess)
