@@ -52,7 +52,19 @@ struct FusedTables {
   float2* t1024 = nullptr;   // W_1024^m, m < 1024
 };
 
-__device__ uint32_t g_fused_dbg = 0;   // fault-bisection knobs (0 in production)
+__device__ uint32_t g_fused_dbg = 0;                  // instrumentation knobs (0 in production)
+__device__ unsigned long long g_fused_ts[2048 * 8];   // per-CTA phase timestamps (knob 128)
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define FGC_TS(k)                                                                        \
+  do {                                                                                   \
+    if ((dbg & 128u) && threadIdx.x == 0 && blockIdx.x < 2048)                           \
+      g_fused_ts[blockIdx.x * 8 + (k)] = globaltimer();                                  \
+  } while (0)
 
 namespace {
 
@@ -91,10 +103,11 @@ __global__ void k_init_tables(float2* thi, float2* tlo, float2* t1024) {
 
 template <class T> struct In;
 template <> struct In<float> {
-  __device__ static float2 get(const float* g, uint64_t e, int half, uint32_t& bad) {
+  template <bool HALF>
+  __device__ static float2 get(const float* g, uint64_t e, uint32_t& bad) {
     float2 v = __ldg(reinterpret_cast<const float2*>(g + e));
     bad |= (isfinite(v.x) && isfinite(v.y)) ? 0u : FGC_FLAG_NONFINITE;
-    if (half) {
+    if (HALF) {
       v.x = __half2float(__float2half_rn(v.x));
       v.y = __half2float(__float2half_rn(v.y));
       bad |= (isinf(v.x) || isinf(v.y)) ? FGC_FLAG_HALF_OVERFLOW : 0u;
@@ -103,11 +116,12 @@ template <> struct In<float> {
   }
 };
 template <> struct In<double> {
-  __device__ static float2 get(const double* g, uint64_t e, int half, uint32_t& bad) {
+  template <bool HALF>
+  __device__ static float2 get(const double* g, uint64_t e, uint32_t& bad) {
     const double2 d = __ldg(reinterpret_cast<const double2*>(g + e));
     if (!isfinite(d.x) || !isfinite(d.y)) { bad |= FGC_FLAG_NONFINITE; return make_float2(0.f, 0.f); }
     float2 v;
-    if (half) {
+    if (HALF) {
       v = make_float2(__half2float(__double2half(d.x)), __half2float(__double2half(d.y)));
       if (isinf(v.x) || isinf(v.y)) bad |= FGC_FLAG_HALF_OVERFLOW;
     } else {
@@ -133,7 +147,6 @@ struct CompressArgs {
   const ChunkInfo* chunks;
   uint32_t first;
   const void* grad;
-  int half;
   QuantParams q;
   uint8_t* message;
   uint32_t* flags;
@@ -146,17 +159,18 @@ struct CompressArgs {
 };
 
 struct __align__(16) CompressShared {
-  float2 buf[kPadded + 64];          // FFT transposes / 4 sub-histograms / bin-ordered code half
+  float2 buf[kPadded + 64];          // FFT transposes / 4 sub-histograms / bin-ordered code half + staging
   float2 thi[256], tlo[256];
   float2 t1024[1024];
-  uint32_t hist[2048];               // merged histogram of this CTA (read by the peer)
+  uint32_t hist[2048];               // pass-1 histogram of this CTA (read by the peer)
+  uint32_t hist2[2048];              // pass-2 histogram of this CTA (read by the peer)
   uint32_t scan[40];
   unsigned long long ckey[kCand];    // CTA 0: undecided bins (exact key, bin)
   uint32_t cidx[kCand];
   uint32_t ccount;                   // CTA 0: number of undecided bins
   uint32_t below;                    // per CTA: bins certainly dropped
   uint32_t anynz;                    // per CTA: any non-zero coefficient
-  uint32_t total;                    // per CTA: codes in its half of the stream
+  uint32_t rcount[2];                // per CTA: its non-zero codes landing in half 0 / half 1
   uint32_t fbin, fbelow;             // merged_bucket result
   int mode;                          // CTA 0's decision, read by CTA 1
   uint32_t need;
@@ -165,15 +179,13 @@ struct __align__(16) CompressShared {
 enum : int { kModeKeepAll = 0, kModeDropAll = 1, kModeList = 2, kModeFallback = 3 };
 
 // Bucket holding rank r in the cluster-merged histogram (own + peer).
-__device__ void merged_bucket(CompressShared& sh, const uint32_t* peer_hist, uint32_t r, uint32_t& bucket,
-                              uint32_t& below) {
+__device__ void merged_bucket(CompressShared& sh, const uint32_t* own, const uint32_t* peer, uint32_t r,
+                              uint32_t& bucket, uint32_t& below) {
   const uint32_t t = threadIdx.x;
-  uint32_t h[4], local = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    h[q] = sh.hist[4 * t + q] + peer_hist[4 * t + q];
-    local += h[q];
-  }
+  const uint4 a = reinterpret_cast<const uint4*>(own)[t];
+  const uint4 b = reinterpret_cast<const uint4*>(peer)[t];
+  const uint32_t h[4] = {a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w};
+  const uint32_t local = h[0] + h[1] + h[2] + h[3];
   uint32_t total;
   const uint32_t before = block_exclusive_scan<kThreads>(local, sh.scan, total);
   if (r >= before && r < before + local) {
@@ -190,17 +202,6 @@ __device__ void merged_bucket(CompressShared& sh, const uint32_t* peer_hist, uin
   __syncthreads();
   bucket = sh.fbin;
   below = sh.fbelow;
-}
-
-// sub-histograms (one per warp quad) in the free FFT buffer -> merged hist
-__device__ __forceinline__ uint32_t* subhist(CompressShared& sh) { return reinterpret_cast<uint32_t*>(sh.buf); }
-__device__ __forceinline__ void zero_subhist(CompressShared& sh) {
-  uint4* s = reinterpret_cast<uint4*>(sh.buf);
-  for (uint32_t e = threadIdx.x; e < 4 * 2048 / 4; e += kThreads) s[e] = make_uint4(0, 0, 0, 0);
-}
-__device__ __forceinline__ void merge_subhist(CompressShared& sh) {
-  const uint32_t* s = subhist(sh);
-  for (uint32_t b = threadIdx.x; b < 2048; b += kThreads) sh.hist[b] = s[b] + s[2048 + b] + s[4096 + b] + s[6144 + b];
 }
 
 // Rare paths kept out of line so the 32-way unrolled per-bin loops stay small
@@ -222,6 +223,52 @@ __device__ __noinline__ void push_candidate(CompressShared* sh0, uint32_t bin, f
   }
 }
 
+// CTA 0: sort the undecided bins by (exact key, bin), mark the `need`
+// smallest dropped, re-sort by bin for the lookups.
+__device__ __noinline__ void resolve_candidates(CompressShared& sh, uint32_t m, uint32_t need) {
+  const uint32_t tid = threadIdx.x;
+  uint32_t M2 = 1;
+  while (M2 < m) M2 <<= 1;
+  for (uint32_t s = m + tid; s < M2; s += kThreads) {
+    sh.ckey[s] = ~0ull;
+    sh.cidx[s] = 0x7FFFFFFFu;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    for (uint32_t k = 2; k <= M2; k <<= 1) {
+      for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+        for (uint32_t t = tid; t < M2; t += kThreads) {
+          const uint32_t u = t ^ jj;
+          if (u > t) {
+            const bool asc = (t & k) == 0;
+            bool gt;
+            if (pass == 0) {
+              gt = sh.ckey[t] > sh.ckey[u] ||
+                   (sh.ckey[t] == sh.ckey[u] && (sh.cidx[t] & 0x7FFFFFFFu) > (sh.cidx[u] & 0x7FFFFFFFu));
+            } else {
+              gt = (sh.cidx[t] & 0x7FFFFFFFu) > (sh.cidx[u] & 0x7FFFFFFFu);
+            }
+            if (gt == asc) {
+              const unsigned long long tk = sh.ckey[t]; sh.ckey[t] = sh.ckey[u]; sh.ckey[u] = tk;
+              const uint32_t ti = sh.cidx[t]; sh.cidx[t] = sh.cidx[u]; sh.cidx[u] = ti;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (pass == 0) {
+      for (uint32_t s = tid; s < need && s < m; s += kThreads) sh.cidx[s] |= 0x80000000u;
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ void zero_buf(CompressShared& sh, uint32_t words4) {
+  uint4* z = reinterpret_cast<uint4*>(sh.buf);
+  for (uint32_t e = threadIdx.x; e < words4; e += kThreads) z[e] = make_uint4(0, 0, 0, 0);
+}
+
 template <class T, bool DEBUG, bool HALF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused_compress(CompressArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -235,28 +282,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   CompressShared& shp = *cluster.map_shared_rank(&sh, r ^ 1);
   const QuantParams q = a.q;
   const uint32_t dbg = g_fused_dbg;
+  const T* g = static_cast<const T*>(a.grad) + ci.in_off;
 
+  if (tid == 0) {
+    // stream this CTA's half of the chunk into L2 while the tables load
+    const uint32_t half_bytes = (uint32_t)(kL / 2 * sizeof(T));
+    const char* base = reinterpret_cast<const char*>(g) + (uint64_t)r * half_bytes;
+    for (uint32_t off = 0; off < half_bytes; off += 32768u)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off), "r"(32768u) : "memory");
+  }
   if (tid < 256) {
     sh.thi[tid] = a.thi[tid];
     sh.tlo[tid] = a.tlo[tid];
   }
   sh.t1024[tid] = a.t1024[tid];
   sh.t1024[tid + 512] = a.t1024[tid + 512];
-  if (tid == 0) { sh.ccount = 0; sh.below = 0; sh.anynz = 0; }
+  reinterpret_cast<uint4*>(sh.hist2)[tid] = make_uint4(0, 0, 0, 0);
+  if (tid == 0) { sh.ccount = 0; sh.below = 0; sh.anynz = 0; sh.rcount[0] = 0; sh.rcount[1] = 0; }
   uint32_t* codes_g = DEBUG ? nullptr : reinterpret_cast<uint32_t*>(a.message + ci.seg_off + ci.code_off);
   __syncthreads();
 
+  FGC_TS(0);
   // ---- 1. load + decimation-in-frequency split (pass-1 input layout)
   float2 v[32];
   {
-    const T* g = static_cast<const T*>(a.grad) + ci.in_off;
     uint32_t bad = 0;
     const float2 wi = tw(sh.thi, sh.tlo, 2u * tid);          // W_N^tid
     static_for<0, 32>([&](auto J) {
       constexpr int j = decltype(J)::value;
       const uint32_t n = tid + 512u * j;
-      const float2 z0 = In<T>::get(g, 2ull * n, HALF, bad);
-      const float2 z1 = In<T>::get(g, 2ull * (n + kM), HALF, bad);
+      const float2 z0 = In<T>::template get<HALF>(g, 2ull * n, bad);
+      const float2 z1 = In<T>::template get<HALF>(g, 2ull * (n + kM), bad);
       if (r == 0) {
         v[j] = make_float2(z0.x + z1.x, z0.y + z1.y);
       } else {                                              // (z0 - z1) W_N^(tid + 512 j)
@@ -266,8 +322,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     if (bad && r == 0) atomicOr(a.flags, bad);
   }
 
+  FGC_TS(1);
   // ---- 2. 16384-point FFT: passes 1, 2 (transposes in smem), pass 3 on two columns
   fft_pass12<false>(v, sh.buf, sh.t1024);
+  FGC_TS(2);
   __syncthreads();
   const bool special = (r == 0 && tid == 0);
   const uint32_t ka = tid;
@@ -329,17 +387,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     return;
   }
 
-  // ---- 4. count-mode selection, cluster-wide
+  FGC_TS(3);
+  // ---- 4. count-mode selection, cluster-wide (cluster barriers A-D)
   const uint32_t kdrop = ci.drop;
   int mode = kModeList;
   if (kdrop == 0) mode = kModeKeepAll;
   else if (kdrop >= kBins) mode = kModeDropAll;
   float band_lo = 0.f, band_hi = INFINITY;
-  uint32_t* sub = subhist(sh) + 2048u * ((tid >> 5) & 3u);
+  uint32_t mcount = 0;
+  __syncthreads();                                // pass-3 reads of buf are done
   if (mode == kModeList) {
-    // pass 1: proxy bits [30:20]
-    __syncthreads();                              // pass-3 reads of buf are done
-    zero_subhist(sh);
+    // pass 1: proxy bits [30:20] into four sub-histograms (in buf)
+    uint32_t* sub = reinterpret_cast<uint32_t*>(sh.buf) + 2048u * ((tid >> 5) & 3u);
+    zero_buf(sh, 2048);
     __syncthreads();
     uint32_t nz = 0;
 #pragma unroll
@@ -348,46 +408,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       const uint32_t pb = __float_as_uint(proxy_key(vb[j].x, vb[j].y));
       nz |= __float_as_uint(va[j].x) | __float_as_uint(va[j].y) | __float_as_uint(vb[j].x) |
             __float_as_uint(vb[j].y);
-      FGC_CHECK((pa >> 20) < 2048u && (pb >> 20) < 2048u);
       atomicAdd(&sub[pa >> 20], 1u);
       atomicAdd(&sub[pb >> 20], 1u);
     }
     if (special) {
-      const uint32_t pn = __float_as_uint(proxy_key(xn.x, xn.y));
       nz |= __float_as_uint(xn.x) | __float_as_uint(xn.y);
-      atomicAdd(&sub[pn >> 20], 1u);
+      atomicAdd(&sub[__float_as_uint(proxy_key(xn.x, xn.y)) >> 20], 1u);
     }
     nz &= 0x7FFFFFFFu;                            // -0.0 is zero
     if (__any_sync(0xffffffffu, nz != 0) && (tid & 31) == 0) atomicOr(&sh.anynz, 1u);
     __syncthreads();
-    merge_subhist(sh);
-    cluster.sync();
+    {
+      const uint4* s4 = reinterpret_cast<const uint4*>(sh.buf);
+      const uint4 x0 = s4[tid], x1 = s4[512 + tid], x2 = s4[1024 + tid], x3 = s4[1536 + tid];
+      reinterpret_cast<uint4*>(sh.hist)[tid] =
+          make_uint4(x0.x + x1.x + x2.x + x3.x, x0.y + x1.y + x2.y + x3.y, x0.z + x1.z + x2.z + x3.z,
+                     x0.w + x1.w + x2.w + x3.w);
+    }
+    cluster.sync();                               // A: pass-1 histograms visible
     const bool anynz = (sh.anynz | shp.anynz) != 0;
     uint32_t b1, below1;
-    merged_bucket(sh, shp.hist, kdrop - 1, b1, below1);
-    cluster.sync();                               // peer finished reading my histogram
+    merged_bucket(sh, sh.hist, shp.hist, kdrop - 1, b1, below1);
     if (!anynz) {
       mode = kModeDropAll;                        // every coefficient is exactly zero: all codes 0
     } else {
-      zero_subhist(sh);
-      __syncthreads();
-      // pass 2: proxy bits [19:9] inside bucket b1
+      // pass 2: proxy bits [19:9] of the bins inside bucket b1 (few: direct atomics)
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const uint32_t pa = __float_as_uint(proxy_key(va[j].x, va[j].y));
         const uint32_t pb = __float_as_uint(proxy_key(vb[j].x, vb[j].y));
-        if ((pa >> 20) == b1) atomicAdd(&sub[(pa >> 9) & 0x7FFu], 1u);
-        if ((pb >> 20) == b1) atomicAdd(&sub[(pb >> 9) & 0x7FFu], 1u);
+        if ((pa >> 20) == b1) atomicAdd(&sh.hist2[(pa >> 9) & 0x7FFu], 1u);
+        if ((pb >> 20) == b1) atomicAdd(&sh.hist2[(pb >> 9) & 0x7FFu], 1u);
       }
       if (special) {
         const uint32_t pn = __float_as_uint(proxy_key(xn.x, xn.y));
-        if ((pn >> 20) == b1) atomicAdd(&sub[(pn >> 9) & 0x7FFu], 1u);
+        if ((pn >> 20) == b1) atomicAdd(&sh.hist2[(pn >> 9) & 0x7FFu], 1u);
       }
       __syncthreads();
-      merge_subhist(sh);
-      cluster.sync();
+    }
+    zero_buf(sh, (kPadded + 64) / 2);             // code arrays: sub-histograms are merged
+    cluster.sync();                               // B: pass-2 histograms visible, buf zeroed
+    if (mode == kModeList) {
       uint32_t b2, below2;
-      merged_bucket(sh, shp.hist, kdrop - 1 - below1, b2, below2);
+      merged_bucket(sh, sh.hist2, shp.hist2, kdrop - 1 - below1, b2, below2);
       const uint32_t lo_pat = (b1 << 20) | (b2 << 9);
       const float lo_f = __uint_as_float(lo_pat);
       const float hi_f = __uint_as_float(lo_pat + 512u);
@@ -412,64 +475,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         const uint32_t bl = block_sum<kThreads>(below_l, sh.scan);
         if (tid == 0) sh.below = bl;
       }
-      cluster.sync();
-      // CTA 0 resolves the undecided bins exactly
-      if (r == 0) {
-        if (tid == 0) {
-          int md = mode;
-          const uint32_t m = sh.ccount;
-          const uint32_t below = sh.below + shp.below;
-          if (md == kModeList && (m > (uint32_t)kCand || below > kdrop || below + m < kdrop)) md = kModeFallback;
-          sh.need = kdrop - below;
-          sh.mode = md;
-        }
-        __syncthreads();
-        mode = sh.mode;
-        if (mode == kModeList) {
-          const uint32_t m = sh.ccount, need = sh.need;
-          uint32_t M2 = 1;
-          while (M2 < m) M2 <<= 1;
-          for (uint32_t s = m + tid; s < M2; s += kThreads) {
-            sh.ckey[s] = ~0ull;
-            sh.cidx[s] = 0x7FFFFFFFu;
-          }
-          __syncthreads();
-          // sort by (key, bin), mark the `need` smallest dropped, then sort by bin
-          for (int pass = 0; pass < 2; ++pass) {
-            for (uint32_t k = 2; k <= M2; k <<= 1) {
-              for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-                for (uint32_t t = tid; t < M2; t += kThreads) {
-                  const uint32_t u = t ^ jj;
-                  if (u > t) {
-                    const bool asc = (t & k) == 0;
-                    bool gt;
-                    if (pass == 0) {
-                      gt = sh.ckey[t] > sh.ckey[u] ||
-                           (sh.ckey[t] == sh.ckey[u] && (sh.cidx[t] & 0x7FFFFFFFu) > (sh.cidx[u] & 0x7FFFFFFFu));
-                    } else {
-                      gt = (sh.cidx[t] & 0x7FFFFFFFu) > (sh.cidx[u] & 0x7FFFFFFFu);
-                    }
-                    if (gt == asc) {
-                      const unsigned long long tk = sh.ckey[t]; sh.ckey[t] = sh.ckey[u]; sh.ckey[u] = tk;
-                      const uint32_t ti = sh.cidx[t]; sh.cidx[t] = sh.cidx[u]; sh.cidx[u] = ti;
-                    }
-                  }
-                }
-                __syncthreads();
-              }
-            }
-            if (pass == 0) {
-              for (uint32_t s = tid; s < need && s < m; s += kThreads) sh.cidx[s] |= 0x80000000u;
-              __syncthreads();
-            }
-          }
-        }
-      }
-      cluster.sync();
-      mode = sh0.mode;
     }
+    cluster.sync();                               // C: candidates and counts visible
+    if (r == 0) {
+      if (tid == 0) {
+        int md = mode;
+        const uint32_t m = sh.ccount;
+        const uint32_t below = sh.below + shp.below;
+        if (md == kModeList && (m > (uint32_t)kCand || below > kdrop || below + m < kdrop)) md = kModeFallback;
+        sh.need = kdrop - below;
+        sh.mode = md;
+      }
+      __syncthreads();
+      if (sh.mode == kModeList) resolve_candidates(sh, sh.ccount, sh.need);
+    }
+    cluster.sync();                               // D: decisions visible
+    mode = sh0.mode;
+    mcount = (mode == kModeList) ? sh0.ccount : 0u;
+  } else {
+    zero_buf(sh, (kPadded + 64) / 2);
+    cluster.sync();                               // D': both code arrays zeroed
   }
 
+  FGC_TS(4);
   if (mode == kModeFallback) {
     float2* out = a.fb_spec + ci.bin_off;
 #pragma unroll
@@ -479,36 +507,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     }
     if (special) out[kN] = xn;
     if (r == 0 && tid == 0) a.fb[chunk] = 1u;
-    cluster.sync();          // keep both CTAs resident until all DSMEM traffic is done
+    cluster.sync();          // peer finished reading sh0.mode before anyone exits
     return;
   }
   if (r == 0 && tid == 0) a.fb[chunk] = 0u;
 
   // ---- 5. codes -> two bin-ordered halves: CTA 0 holds bins [0, 16384),
-  //         CTA 1 holds [16384, 32768]; each zero-fills its half first.
-  __syncthreads();                              // buf (sub-histograms) no longer read
-  {
-    uint4* z = reinterpret_cast<uint4*>(sh.buf);
-    for (uint32_t e = tid; e < (kPadded + 64) / 2; e += kThreads) z[e] = make_uint4(0, 0, 0, 0);
-  }
-  cluster.sync();
-  const uint32_t mcount = (mode == kModeList) ? sh0.ccount : 0u;
-  uint32_t* arr_own = reinterpret_cast<uint32_t*>(sh.buf);
-  uint32_t* arr_peer = reinterpret_cast<uint32_t*>(shp.buf);
-  // band in the proxy domain; KeepAll / DropAll become degenerate bands
-  float lo_b = band_lo, hi_b = band_hi;
+  //         CTA 1 holds [16384, 32768]; non-zero pairs only (arrays are zeroed).
+  float lo_b = band_lo, hi_b = band_hi;           // KeepAll / DropAll as degenerate bands
   if (mode == kModeKeepAll) { lo_b = -1.0f; hi_b = -1.0f; }
   if (mode == kModeDropAll) { lo_b = INFINITY; hi_b = INFINITY; }
+  uint32_t* arr_own = reinterpret_cast<uint32_t*>(sh.buf);
+  uint32_t* arr_peer = reinterpret_cast<uint32_t*>(shp.buf);
+  uint32_t rc0 = 0, rc1 = 0;                      // my non-zero codes per half
   auto emit_pair = [&](float2 x, uint32_t bin) {
     const float p = proxy_key(x.x, x.y);
     bool keep = p >= lo_b;
     if (keep && p < hi_b) keep = !inband_dropped(&sh0, mcount, bin);
     if (keep) {
-      const uint32_t pc = enc16(q, x.x) | (enc16(q, x.y) << 16);
+      const uint32_t cre = enc16(q, x.x), cim = enc16(q, x.y);
+      const uint32_t pc = cre | (cim << 16);
       if (pc) {
         const uint32_t d = bin >= kHalfBins ? 1u : 0u;
+        const uint32_t c = (cre ? 1u : 0u) + (cim ? 1u : 0u);
+        if (d) rc1 += c; else rc0 += c;
         uint32_t* dst = (d == r) ? arr_own : arr_peer;
-        FGC_CHECK(bin <= kN && pad(bin - d * kHalfBins) < 2u * (kPadded + 64));
         dst[pad(bin - d * kHalfBins)] = pc;
       }
     }
@@ -519,21 +542,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     emit_pair(vb[j], BIN_B(j));
   }
   if (special) emit_pair(xn, kN);
-  cluster.sync();
 #undef BIN_A
 #undef BIN_B
-  if (dbg & 8u) {
-    cluster.sync();
-    return;
+  {
+    const uint32_t s0 = __reduce_add_sync(0xffffffffu, rc0), s1 = __reduce_add_sync(0xffffffffu, rc1);
+    if ((tid & 31) == 0) {
+      if (s0) atomicAdd(&sh.rcount[0], s0);
+      if (s1) atomicAdd(&sh.rcount[1], s1);
+    }
   }
+  cluster.sync();                                 // E: both halves complete, per-half counts visible
+  FGC_TS(5);
+  const uint32_t t0 = sh.rcount[0] + shp.rcount[0];            // codes in half 0
+  const uint32_t all = t0 + sh.rcount[1] + shp.rcount[1];       // codes in the chunk
+  const int N = q.n_bits;
+  // byte-aligned half boundary (N = 8, 16, or t0*N % 8 == 0): no cross-CTA fold needed
+  const uint64_t s1bits = (uint64_t)t0 * N;
+  const bool fold = (s1bits & 7u) != 0;
+  // Without a fold this was the last remote access: arrive now, wait before
+  // exiting (a CTA's shared memory must outlive its peer's accesses).
+  if (!fold) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 
   // ---- 6. pack: thread t of CTA d owns bins d*16384 + [32t, 32t+32) (+ bin N)
-  const int N = q.n_bits;
   const uint32_t nb = (r == 1 && tid == kThreads - 1) ? 33u : 32u;
   uint32_t w0 = 0, w1 = 0, w2 = 0;
-  uint32_t cnt = 0;
   {
-    const uint32_t* src = arr_own + pad(32u * tid);    // 32 entries + pad: pad(32t + j) = pad(32t) + j
+    const uint32_t* src = arr_own + pad(32u * tid);    // pad(32t + j) = pad(32t) + j
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const uint32_t pc = src[j];
@@ -545,8 +579,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       const uint32_t pc = arr_own[pad(32u * tid + 32u)];
       w2 = ((pc & 0xFFFFu) ? 1u : 0u) | ((pc >> 16) ? 2u : 0u);
     }
-    cnt = __popc(w0) + __popc(w1) + __popc(w2);
   }
+  const uint32_t cnt = __popc(w0) + __popc(w1) + __popc(w2);
   uint32_t* seg = reinterpret_cast<uint32_t*>(a.message + ci.seg_off);
   uint32_t* bm = seg + kSegHeader / 4;
   {
@@ -561,30 +595,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   }
   uint32_t total;
   const uint32_t base = block_exclusive_scan<kThreads>(cnt, sh.scan, total);
-  if (tid == 0) sh.total = total;
-  cluster.sync();
-  const uint32_t t0 = sh0.total;                         // codes in CTA 0's half
-  const uint32_t all = t0 + shp.total * (1u - r) + total * r;   // t0 + t1
-  // This CTA's half of the stream starts at global bit S = (r ? t0 : 0) * N.
-  // It is assembled in a shared staging area (after the code array in buf):
-  // local word k <-> global word (S >> 5) + k; bit offset o = S & 31.
-  const uint64_t S = (uint64_t)(r ? t0 : 0u) * N;
+  // This CTA's half of the stream starts at global bit S = (r ? t0 : 0) * N;
+  // staged in shared memory: local word k <-> global word (S >> 5) + k.
+  const uint64_t S = r ? s1bits : 0ull;
   const uint32_t wstart = (uint32_t)(S >> 5), o = (uint32_t)(S & 31u);
   const uint32_t nwords = (uint32_t)((o + (uint64_t)total * N + 31) / 32);
   uint32_t* stg = arr_own + kStageOff;
   for (uint32_t k = tid; k < nwords; k += kThreads) stg[k] = 0u;
   __syncthreads();
   {
-    uint64_t lbit = o + (uint64_t)base * N;              // local bit position of my first code
+    uint64_t lbit = o + (uint64_t)base * N;               // local bit of my first code
     auto emit_word_bits = [&](uint32_t word, uint32_t jbase) {
       while (word) {
         const uint32_t pos = __ffs(word) - 1;
         word &= word - 1;
         const uint32_t pc = arr_own[pad(32u * tid + jbase + (pos >> 1))];
         const uint32_t code = (pos & 1) ? (pc >> 16) : (pc & 0xFFFFu);
-        const uint32_t wi = (uint32_t)(lbit >> 5), sh_ = (uint32_t)(lbit & 31u);
-        atomicOr(&stg[wi], code << sh_);
-        if (sh_ + N > 32u) atomicOr(&stg[wi + 1], code >> (32u - sh_));
+        const uint32_t wi = (uint32_t)(lbit >> 5), sb = (uint32_t)(lbit & 31u);
+        atomicOr(&stg[wi], code << sb);
+        if (sb + N > 32u) atomicOr(&stg[wi + 1], code >> (32u - sb));
         lbit += N;
       }
     };
@@ -593,29 +622,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     emit_word_bits(w2, 32);
   }
   __syncthreads();
-  cluster.sync();          // both halves staged
-  // CTA 1's first word is shared with CTA 0's last one when t0*N is not word
-  // aligned: CTA 0 folds it in and owns that word.
-  if (r == 0 && tid == 0) {
-    const uint64_t s1 = (uint64_t)t0 * N;
-    if (s1 & 31u) stg[s1 >> 5] |= (reinterpret_cast<const uint32_t*>(shp.buf) + kStageOff)[0];
+  if (fold) {
+    // the half boundary splits a byte: CTA 0 folds CTA 1's first word and owns it
+    cluster.sync();                               // F: CTA 1's staging complete
+    if (r == 0 && tid == 0) stg[s1bits >> 5] |= (reinterpret_cast<const uint32_t*>(shp.buf) + kStageOff)[0];
+    __syncthreads();
   }
-  __syncthreads();
-  // coalesced write-out (CTA 0 owns the shared word); zero the unused capacity
-  const uint32_t first = (r == 1 && o != 0) ? 1u : 0u;
+  // write-out; the word shared by the two halves is written bytewise by each owner
+  const uint32_t shared_w = (uint32_t)(s1bits >> 5);
+  const bool split = (s1bits & 31u) != 0 && !fold;
+  for (uint32_t k = tid; k < nwords; k += kThreads) {
+    const uint32_t w = wstart + k;
+    if (w >= ci.code_cap) continue;
+    if (r == 1 && fold && k == 0) continue;       // folded into CTA 0's copy
+    if (split && w == shared_w) {
+      uint8_t* p = reinterpret_cast<uint8_t*>(codes_g + w);
+      const uint32_t bb = (uint32_t)(s1bits & 31u) >> 3;       // bytes [0, bb) belong to half 0
+      const uint32_t val = stg[k];
+      for (uint32_t b = (r ? bb : 0u); b < (r ? 4u : bb); ++b) p[b] = (uint8_t)(val >> (8 * b));
+      continue;
+    }
+    codes_g[w] = stg[k];
+  }
   const uint32_t used = (uint32_t)(((uint64_t)all * N + 31) / 32);
   const uint32_t cap_padded = (ci.code_cap + 3u) & ~3u;
-  for (uint32_t k = first + tid; k < nwords; k += kThreads) {
-    if (wstart + k < ci.code_cap) codes_g[wstart + k] = stg[k];
-  }
   if (r == 1)
     for (uint32_t w = used + tid; w < cap_padded; w += kThreads) codes_g[w] = 0u;
-  if (r == 1 && tid == 0) {
+  if (r == 0 && tid == 0) {
     seg[0] = all;
     seg[1] = 0; seg[2] = 0; seg[3] = 0;
     if (used > ci.code_cap) atomicOr(a.flags, FGC_FLAG_CAPACITY);
   }
-  cluster.sync();          // peers finished their DSMEM reads; keep both resident until done
+  if (fold) cluster.sync();                       // G: CTA 0 finished reading CTA 1's staging
+  else asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  FGC_TS(6);
 }
 
 // ------------------------------------------------------------------ decode
@@ -644,8 +684,7 @@ struct __align__(16) DecodeShared {
   uint32_t scan[40];
 };
 
-// Add the contributions of bin b's (weighted) value X to Y_r.
-// wb = W_L^b.
+// Add the contributions of bin b's (weighted) value X to Y_r; wb = W_L^b.
 __device__ __forceinline__ void scatter_bin(DecodeShared& sh, uint32_t r, uint32_t b, float2 X, float2 wb) {
   float2 cA = make_float2(0.5f * (1.0f + wb.y), 0.5f * wb.x);   // (1 + i W_L^-b)/2
   float2 cB = make_float2(0.5f * (1.0f - wb.y), 0.5f * wb.x);   // (1 + i W_L^b)/2
@@ -789,9 +828,13 @@ bool fused_available() { return true; }
 
 }  // namespace fgc
 
-// Internal fault-bisection hook (not part of the public header).
+// Internal instrumentation hooks (not part of the public header).
 extern "C" int fgc_debug_set_fused_knobs(uint32_t knobs) {
   return cudaMemcpyToSymbol(fgc::g_fused_dbg, &knobs, sizeof(knobs)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int fgc_debug_fused_timestamps(unsigned long long* host, uint32_t count) {
+  if (count > 2048 * 8) count = 2048 * 8;
+  return cudaMemcpyFromSymbol(host, fgc::g_fused_ts, count * sizeof(unsigned long long)) == cudaSuccess ? 0 : 1;
 }
 
 namespace fgc {
@@ -838,7 +881,7 @@ static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_
                                        const QuantParams& q, uint8_t* message, uint32_t* flags, uint32_t* fb,
                                        float2* fb_spec, float2* dbg, cudaStream_t s) {
   if (!count) return FGC_OK;
-  CompressArgs a{d_chunks, first, grad, half_pass, q, message, flags, t->thi, t->tlo, t->t1024, fb, fb_spec, dbg};
+  CompressArgs a{d_chunks, first, grad, q, message, flags, t->thi, t->tlo, t->t1024, fb, fb_spec, dbg};
   const size_t smem = sizeof(CompressShared);
   const dim3 grid(2 * count), block(kThreads);
   const bool f64 = dtype == FGC_DTYPE_F64, h = half_pass != 0;
