@@ -34,7 +34,7 @@ __all__ = [
     "drop_set", "Chunk", "Message", "chunk_lengths", "slot_count",
     "encode_spectrum", "compress", "decompress", "reconstruct_rows",
     "average", "to_wire", "from_wire", "calibrate", "WireError",
-    "keep_bins", "device_layout", "device_segments", "DEFAULT_CHUNK",
+    "keep_bins", "device_layout", "device_segments", "from_device", "DEFAULT_CHUNK",
 ]
 
 DEFAULT_CHUNK = 1 << 16          # codec.py:73
@@ -549,6 +549,23 @@ def device_layout(n: int, chunk: int, theta: float, width: int, mode: str = "cou
         out.append((off, 16, code_off, cap))
         off += cap
     return out, off
+
+
+def from_device(buf: bytes, n: int, chunk: int, theta: float, lat: Lattice | None,
+                mode: str = "count", half: bool = False) -> Message:
+    """Parse a fixed-capacity device message back into a Message."""
+    width = 32 if lat is None else lat.n_bits
+    layout, total = device_layout(n, chunk, theta, width, mode)
+    if len(buf) < total:
+        raise ValueError("device message shorter than its layout")
+    chunks = []
+    for (off, bmo, co, cap), length in zip(layout, chunk_lengths(n, chunk)):
+        slots = slot_count(length)
+        nnz = struct.unpack_from("<I", buf, off)[0]
+        bm = bytes_to_flags(buf[off + bmo: off + bmo + (slots + 7) // 8], slots)
+        cb = (nnz * width + 7) // 8
+        chunks.append(Chunk(bm, bytes_to_codes(buf[off + co: off + co + cb], width, nnz)))
+    return Message(n, chunk, float(np.float32(theta)), mode, half, lat, chunks)
 
 
 def device_segments(msg: Message, theta: float) -> bytes:
