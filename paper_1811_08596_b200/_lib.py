@@ -11,7 +11,9 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libfgc_b200.so"
+# FGC_LIB_VARIANT=x loads libfgc_b200.x.so (A/B builds of the same tree)
+LIB_PATH = _HERE / ("libfgc_b200.%s.so" % os.environ["FGC_LIB_VARIANT"]
+                    if os.environ.get("FGC_LIB_VARIANT") else "libfgc_b200.so")
 
 OK = 0
 ERR_INVALID, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL = 1, 2, 3, 4

@@ -53,7 +53,7 @@ struct FusedTables {
 };
 
 __device__ uint32_t g_fused_dbg = 0;                  // instrumentation knobs (0 in production)
-__device__ unsigned long long g_fused_ts[2048 * 8];   // per-CTA phase timestamps (knob 128)
+__device__ unsigned long long g_fused_ts[2048 * 16];   // per-CTA phase timestamps (knob 128)
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -63,7 +63,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #define FGC_TS(k)                                                                        \
   do {                                                                                   \
     if ((dbg & 128u) && threadIdx.x == 0 && blockIdx.x < 2048)                           \
-      g_fused_ts[blockIdx.x * 8 + (k)] = globaltimer();                                  \
+      g_fused_ts[blockIdx.x * 16 + (k)] = globaltimer();                                  \
   } while (0)
 
 namespace {
@@ -425,6 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           make_uint4(x0.x + x1.x + x2.x + x3.x, x0.y + x1.y + x2.y + x3.y, x0.z + x1.z + x2.z + x3.z,
                      x0.w + x1.w + x2.w + x3.w);
     }
+    FGC_TS(7);
     cluster.sync();                               // A: pass-1 histograms visible
     const bool anynz = (sh.anynz | shp.anynz) != 0;
     uint32_t b1, below1;
@@ -447,6 +448,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       __syncthreads();
     }
     zero_buf(sh, (kPadded + 64) / 2);             // code arrays: sub-histograms are merged
+    FGC_TS(8);
     cluster.sync();                               // B: pass-2 histograms visible, buf zeroed
     if (mode == kModeList) {
       uint32_t b2, below2;
@@ -476,6 +478,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         if (tid == 0) sh.below = bl;
       }
     }
+    FGC_TS(9);
     cluster.sync();                               // C: candidates and counts visible
     if (r == 0) {
       if (tid == 0) {
@@ -489,6 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       __syncthreads();
       if (sh.mode == kModeList) resolve_candidates(sh, sh.ccount, sh.need);
     }
+    FGC_TS(10);
     cluster.sync();                               // D: decisions visible
     mode = sh0.mode;
     mcount = (mode == kModeList) ? sh0.ccount : 0u;
@@ -551,6 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       if (s1) atomicAdd(&sh.rcount[1], s1);
     }
   }
+  FGC_TS(11);
   cluster.sync();                                 // E: both halves complete, per-half counts visible
   FGC_TS(5);
   const uint32_t t0 = sh.rcount[0] + shp.rcount[0];            // codes in half 0
@@ -833,7 +838,7 @@ extern "C" int fgc_debug_set_fused_knobs(uint32_t knobs) {
   return cudaMemcpyToSymbol(fgc::g_fused_dbg, &knobs, sizeof(knobs)) == cudaSuccess ? 0 : 1;
 }
 extern "C" int fgc_debug_fused_timestamps(unsigned long long* host, uint32_t count) {
-  if (count > 2048 * 8) count = 2048 * 8;
+  if (count > 2048 * 16) count = 2048 * 16;
   return cudaMemcpyFromSymbol(host, fgc::g_fused_ts, count * sizeof(unsigned long long)) == cudaSuccess ? 0 : 1;
 }
 
