@@ -8,6 +8,9 @@
 //   Pow2       Lc = 2^k            Stockham radix-2 in shared memory (<= 4096
 //                                  points), larger sizes by a four-step split
 //                                  through global memory (recursive on rows)
+//   Mixed      Lc = A 2^e, A odd    one direct pass over the odd factor (A <=
+//              <= kMixedMaxA       kMixedMaxA, twiddles folded in) + A Pow2
+//                                  rows of B = 2^e points (Cooley-Tukey)
 //   Bluestein  anything else        chirp-z convolution on a Pow2 engine of
 //                                  size P >= 2 Lc - 1
 //
@@ -174,6 +177,40 @@ __global__ void k_direct_dft(const typename V2<R>::T* in, typename V2<R>::T* out
   }
 }
 
+// Mixed-radix outer pass, Lc = A * B.  Index n = B n1 + n2, k = k1 + A k2.
+//   forward (dir < 0): Y[k1 B + n2] = sum_n1 x[B n1 + n2] W^(k1 (B n1 + n2))
+//                      (then a B-point FFT down each row k1 gives X[k1 + A k2])
+//   inverse (dir > 0): x[B n1 + n2] = sum_k1 Y'[k1 B + n2] W^(-k1 (B n1 + n2))
+//                      (after the B-point inverse FFT of each row k1)
+// W = exp(-2 pi i / Lc) from the exact table mtw.  One thread per output.
+template <class T2>
+__global__ void k_mixed_pass(const T2* in, T2* out, const T2* mtw, uint32_t A, uint32_t B, uint64_t total, int dir) {
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const uint32_t Lc = A * B;
+  const uint64_t item = e / Lc;
+  const uint32_t r = (uint32_t)(e - item * Lc);
+  const uint32_t o = r / B, n2 = r - o * B;         // o = k1 (forward) or n1 (inverse)
+  const T2* src = in + item * Lc + n2;
+  uint32_t m, step;
+  if (dir < 0) {                                     // m = o (B i + n2)
+    m = (uint32_t)(((uint64_t)o * n2) % Lc);
+    step = (uint32_t)(((uint64_t)o * B) % Lc);
+  } else {                                           // m = i (B o + n2)
+    m = 0;
+    step = o * B + n2;
+  }
+  T2 acc = mk(src[0].x * 0, src[0].y * 0);
+  for (uint32_t i = 0; i < A; ++i) {
+    T2 w = mtw[m];
+    if (dir > 0) w.y = -w.y;
+    acc = zadd(acc, zmul(src[(uint64_t)i * B], w));
+    m += step;
+    if (m >= Lc) m -= Lc;
+  }
+  out[e] = acc;
+}
+
 template <class T2>
 __global__ void k_pointwise_mul(T2* data, const T2* f, uint32_t P, uint64_t total) {
   const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -245,19 +282,34 @@ fgc_status DftPlanT<R>::init(uint32_t Lc_, uint32_t batch_, cudaStream_t s) {
   } else if ((Lc & (Lc - 1)) == 0) {
     kind = DftKind::Pow2;
     P = Lc;
+  } else if ((Lc >> __builtin_ctz(Lc)) <= kMixedMaxA) {
+    kind = DftKind::Mixed;
+    B = 1u << __builtin_ctz(Lc);
+    A = Lc / B;
+    P = Lc;
   } else {
     kind = DftKind::Bluestein;
     if (2ull * Lc - 1 > (1ull << 31)) { set_error("DFT length too large"); return FGC_ERR_UNSUPPORTED; }
     P = next_pow2(2ull * Lc - 1);
   }
-  if (kind != DftKind::Direct) {
+  if (kind == DftKind::Mixed) {
+    FGC_CUDA(cudaMalloc(&mtw, sizeof(T2) * Lc));
+    k_init_twiddles<R><<<ceil_div(Lc, 256), 256, 0, s>>>(mtw, Lc);
+    FGC_LAUNCHED(1);
+    if (B > 1) {
+      FGC_CUDA(cudaMalloc(&tw, sizeof(T2) * B));
+      k_init_twiddles<R><<<ceil_div(B, 256), 256, 0, s>>>(tw, B);
+      FGC_LAUNCHED(1);
+    }
+  } else if (kind != DftKind::Direct) {
     FGC_CUDA(cudaMalloc(&tw, sizeof(T2) * P));
     k_init_twiddles<R><<<ceil_div(P, 256), 256, 0, s>>>(tw, P);
     FGC_LAUNCHED(1);
   }
   if (batch) {
     FGC_CUDA(cudaMalloc(&work, sizeof(T2) * (uint64_t)P * batch));
-    if (kind == DftKind::Direct) FGC_CUDA(cudaMalloc(&work2, sizeof(T2) * (uint64_t)P * batch));
+    if (kind == DftKind::Direct || kind == DftKind::Mixed)
+      FGC_CUDA(cudaMalloc(&work2, sizeof(T2) * (uint64_t)P * batch));
   }
   if (kind == DftKind::Bluestein) {
     FGC_CUDA(cudaMalloc(&chirp, sizeof(T2) * Lc));
@@ -279,7 +331,8 @@ void DftPlanT<R>::free_all() {
   cudaFree(work);
   cudaFree(work2);
   cudaFree(rtw);
-  tw = chirp = bf = work = work2 = rtw = nullptr;
+  cudaFree(mtw);
+  tw = chirp = bf = work = work2 = rtw = mtw = nullptr;
 }
 
 template <class R>
@@ -296,6 +349,25 @@ fgc_status DftPlanT<R>::run(int dir, DftResultT<R>& res, cudaStream_t s) {
       FGC_TRY(pow2_rec<R>(work, batch, P, tw, P, dir, s));
       res = DftResultT<R>{work, P, dir < 0 ? 1 : 0, 0};
       return FGC_OK;
+    case DftKind::Mixed: {
+      const uint64_t total = (uint64_t)batch * Lc;
+      if (dir < 0) {                                 // natural work -> rows in work2 (engine layout)
+        if (total) {
+          k_mixed_pass<T2><<<ceil_div(total, 256), 256, 0, s>>>(work, work2, mtw, A, B, total, -1);
+          FGC_LAUNCHED(1);
+        }
+        FGC_TRY(pow2_rec<R>(work2, (uint64_t)batch * A, B, tw, B, -1, s));
+        res = DftResultT<R>{work2, Lc, 2, 0};
+      } else {                                       // rows (engine layout) in work -> natural work2
+        FGC_TRY(pow2_rec<R>(work, (uint64_t)batch * A, B, tw, B, +1, s));
+        if (total) {
+          k_mixed_pass<T2><<<ceil_div(total, 256), 256, 0, s>>>(work, work2, mtw, A, B, total, +1);
+          FGC_LAUNCHED(1);
+        }
+        res = DftResultT<R>{work2, Lc, 0, 0};
+      }
+      return FGC_OK;
+    }
     case DftKind::Bluestein: {
       FGC_TRY(pow2_rec<R>(work, batch, P, tw, P, -1, s));
       const uint64_t total = (uint64_t)batch * P;

@@ -39,7 +39,10 @@ void count_launch(uint64_t n = 1);
 // ---------------------------------------------------------------- generic DFT
 // Complex DFT of length Lc for a batch of signals (fft_generic.cu), in
 // float32 (codec tails) or float64 (whole-signal primitives, calibrate).
-enum class DftKind : int { Direct = 0, Pow2 = 1, Bluestein = 2 };
+enum class DftKind : int { Direct = 0, Pow2 = 1, Bluestein = 2, Mixed = 3 };
+
+// Mixed: Lc = A * B, B = 2^e, A odd <= kMixedMaxA (one direct pass + Pow2 rows).
+constexpr uint32_t kMixedMaxA = 512;
 
 template <class R> struct Vec2;
 template <> struct Vec2<float> { using T = float2; };
@@ -71,11 +74,20 @@ __host__ __device__ inline uint64_t engine_pos(uint32_t P, uint32_t cap, uint64_
   return base + k;
 }
 
+// Where frequency k of a DFT result lives: layout 0 natural, 1 Pow2 engine
+// layout of size P, 2 Mixed rows (k % A) of B points in engine layout.
+__host__ __device__ inline uint64_t result_pos(int layout, uint32_t P, uint32_t A, uint32_t B, uint32_t cap,
+                                               uint64_t k) {
+  if (layout == 1) return engine_pos(P, cap, k);
+  if (layout == 2) return (k % A) * B + engine_pos(B, cap, k / A);
+  return k;
+}
+
 template <class R>
 struct DftResultT {
   const typename Vec2<R>::T* base;  // buffer
   uint64_t stride;                  // per batch item
-  int layout;                       // 0 natural, 1 engine layout
+  int layout;                       // 0 natural, 1 engine layout, 2 mixed rows (result_pos)
   int chirp;                        // 1: multiply by chirp[k] / P (Bluestein)
 };
 
@@ -84,11 +96,13 @@ struct DftPlanT {
   using T2 = typename Vec2<R>::T;
   DftKind kind = DftKind::Direct;
   uint32_t Lc = 1;        // DFT length
-  uint32_t P = 1;         // pow2 transform size (Pow2 / Bluestein); Lc for Direct
+  uint32_t P = 1;         // pow2 transform size (Pow2 / Bluestein); Lc for Direct / Mixed
+  uint32_t A = 1, B = 1;  // Mixed factors (Lc = A * B)
   uint32_t batch = 0;
   T2* tw = nullptr;       // P twiddles exp(-2 pi i j / P)
   T2* chirp = nullptr;    // Bluestein chirp exp(-i pi n^2 / Lc), n < Lc
   T2* bf = nullptr;       // Bluestein kernel spectrum, engine layout
+  T2* mtw = nullptr;      // Mixed: exp(-2 pi i m / Lc), m < Lc
   T2* work = nullptr;     // batch * P
   T2* work2 = nullptr;    // Direct output buffer
   T2* rtw = nullptr;      // real-signal twiddles exp(-2 pi i k / L), k <= L/2 (even L)

@@ -79,7 +79,7 @@ template <class R>
 struct Args {
   using T2 = typename Vec2<R>::T;
   const ChunkInfo* chunks;
-  uint32_t first, L, Lc, Pw, P, bins, cap;
+  uint32_t first, L, Lc, Pw, P, A, B, bins, cap;
   int kind;
   T2* work;
   const T2* chirp;
@@ -116,7 +116,7 @@ struct Res {
 
 template <class R>
 __device__ __forceinline__ typename Vec2<R>::T res_get(const Args<R>& a, const Res<R>& r, uint32_t j, uint64_t k) {
-  const uint64_t pos = r.layout ? engine_pos(a.P, a.cap, k) : k;
+  const uint64_t pos = result_pos(r.layout, a.P, a.A, a.B, a.cap, k);
   typename Vec2<R>::T v = r.base[(uint64_t)j * r.stride + pos];
   if (r.chirp) {
     v = mul2(v, a.chirp[k]);
@@ -183,6 +183,8 @@ __global__ void k_iprep(Args<R> a, const typename Vec2<R>::T* spectrum) {
     if (k < a.Lc) Z = mul2(cj(Z), a.chirp[k]);
   } else if (a.kind == (int)DftKind::Pow2) {
     pos = engine_pos(a.P, a.cap, k);
+  } else if (a.kind == (int)DftKind::Mixed) {
+    pos = result_pos(2, a.P, a.A, a.B, a.cap, k);
   }
   a.work[(uint64_t)j * a.Pw + pos] = Z;
 }
@@ -214,6 +216,8 @@ Args<R> make_args(const RealClassT<R>& rc, const ChunkInfo* d_chunks) {
   a.Lc = d.Lc;
   a.Pw = d.P;
   a.P = d.P;
+  a.A = d.A;
+  a.B = d.B;
   a.bins = rc.bins;
   a.cap = smem_points(sizeof(R));
   a.kind = (int)d.kind;

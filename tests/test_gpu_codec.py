@@ -136,7 +136,10 @@ def test_injection_degenerate_chunks():
 
 # ---------------------------------------------------------------- FFTs
 
+# tails of the benchmark configs: 40960 (5 x 2^12 mixed), 16960 (265 x 2^5 mixed),
+# 46720 (365 x 2^6 mixed), 51520 / 5402 (Bluestein), plus odd and tiny chunks
 @pytest.mark.parametrize("n,chunk", [(1_000_000, 65536), (65536 * 3, 65536), (40960 + 65536, 65536),
+                                     (16960, 65536), (46720, 65536), (51520, 65536), (5402, 65536),
                                      (5000, 1024), (777, 64), (100, 17), (33, 16), (65537, 65536)])
 def test_forward_coefficients_match_float64_rfft(n, chunk):
     rng = np.random.default_rng(n)
@@ -156,7 +159,8 @@ def test_forward_coefficients_match_float64_rfft(n, chunk):
         off += L
 
 
-@pytest.mark.parametrize("n,chunk", [(1_000_000, 65536), (5000, 1024), (777, 64), (101, 17)])
+@pytest.mark.parametrize("n,chunk", [(1_000_000, 65536), (40960 + 65536, 65536), (46720, 65536), (51520, 65536),
+                                     (5000, 1024), (777, 64), (101, 17)])
 def test_inverse_matches_float64_irfft(n, chunk):
     rng = np.random.default_rng(n + 1)
     bins = [L // 2 + 1 for L in O.chunk_lengths(n, chunk)]
@@ -429,7 +433,7 @@ def test_packer_primitives():
 
 def test_spectral_primitives(golden):
     rng = np.random.default_rng(0)
-    for n in [1, 2, 3, 17, 128, 1000, 1024, 4097, 100_003]:
+    for n in [1, 2, 3, 17, 128, 1000, 1024, 4097, 40960, 46720, 100_003]:
         v = rng.standard_normal(n)
         ref = np.fft.rfft(v)
         got = F.dft_forward(v).coefficients
