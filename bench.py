@@ -300,6 +300,13 @@ def run_ours(args, wl, rank, world, local_rank):
     dec_bytes = float(world) * M + 4.0 * n
     dom = ("compress", comp_bytes, c_ms) if c_ms >= d_ms else ("decode_average", dec_bytes, d_ms)
     achieved = dom[1] / (dom[2] * 1e-3) / 1e9
+    traffic = None        # DRAM bytes per launch of that kernel from the committed ncu --set full capture
+    try:
+        tr = json.load(open(Path(__file__).resolve().parent / "profiles" / "traffic.json"))
+        if not args.n and (dom[0] == "compress" or world == 1):
+            traffic = tr.get(args.workload, {}).get(dom[0])
+    except (OSError, ValueError):
+        pass
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -309,7 +316,7 @@ def run_ours(args, wl, rank, world, local_rank):
         "allreduce_fp32_ms": allreduce_ms,
         "message_bytes": M, "compression_ratio": 4.0 * n / M,
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                      "algorithmic_bytes": dom[1],
                      "step_frac": ((comp_bytes + dec_bytes) / ((c_ms + d_ms) * 1e-3) / 1e9) / hbm},
         "e2e": {"value": job_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
