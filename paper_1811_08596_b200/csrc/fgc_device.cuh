@@ -151,6 +151,51 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   return r;
 }
 
+// Four independent exclusive scans at once (one set of barriers).
+// `scratch` holds >= 4 * (THREADS / 32 + 1) words.
+template <int THREADS>
+__device__ __forceinline__ uint4 block_exclusive_scan4(uint4 v, uint32_t* scratch, uint4& total) {
+  static_assert(THREADS % 32 == 0 && THREADS <= 512, "block size");
+  constexpr int WARPS = THREADS / 32, S = WARPS + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x[k], d);
+      if (lane >= d) x[k] += y;
+    }
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) scratch[k * S + warp] = x[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t s = (lane < WARPS) ? scratch[k * S + lane] : 0u;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, s, d);
+        if (lane >= d) s += y;
+      }
+      if (lane < WARPS) scratch[k * S + lane] = s;   // inclusive warp totals; [WARPS-1] = block total
+    }
+  }
+  __syncthreads();
+  uint32_t out[4], tot[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    out[k] = (warp ? scratch[k * S + warp - 1] : 0u) + x[k] - (&v.x)[k];
+    tot[k] = scratch[k * S + WARPS - 1];
+  }
+  total = make_uint4(tot[0], tot[1], tot[2], tot[3]);
+  __syncthreads();
+  return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
 template <int THREADS>
 __device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* scratch) {
   uint32_t total;

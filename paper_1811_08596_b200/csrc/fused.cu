@@ -680,42 +680,72 @@ struct DecodeArgs {
   const float2* spectrum;     // dense-spectrum mode (debug hook), else null
 };
 
+constexpr int kDecBatch = 4;                           // messages per block scan in the decode
+
 struct __align__(16) DecodeShared {
-  float2 y[kPadded + 64];
+  float2 x[kPadded + 64];            // this CTA's bins of the weighted spectrum sum, then Y_r / FFT scratch
   float2 thi[256], tlo[256];
   float2 t1024[1024];
-  uint32_t bm[kBmWords + 3];
-  uint32_t pref[kBmWords + 3];
-  uint32_t scan[40];
+  uint32_t bm[kDecBatch][2 * kThreads * 2];   // natural-order bitmap words 0..2047 of a message batch
+  uint32_t pref[kDecBatch][2 * kThreads];     // codes before each 32-bin block
+  uint32_t bmN[kDecBatch];                    // word 2048 (bin N)
+  uint32_t scan[4 * (kThreads / 32 + 1)];     // block_exclusive_scan4 scratch
 };
 
-// Add the contributions of bin b's (weighted) value X to Y_r; wb = W_L^b.
-__device__ __forceinline__ void scatter_bin(DecodeShared& sh, uint32_t r, uint32_t b, float2 X, float2 wb) {
-  float2 cA = make_float2(0.5f * (1.0f + wb.y), 0.5f * wb.x);   // (1 + i W_L^-b)/2
-  float2 cB = make_float2(0.5f * (1.0f - wb.y), 0.5f * wb.x);   // (1 + i W_L^b)/2
-  if (r) {
-    const float2 w2 = cmul(wb, wb);                             // W_N^b = (W_L^b)^2
-    cA = cmulc(cA, w2);                                         // * W_N^-b
-    cB = cmul(cB, w2);                                          // * W_N^b
-  }
-  if (b < kN) {
-    float2& y = sh.y[pad(b & (kM - 1))];
-    const float2 c = cmul(cA, X);
-    y.x += c.x;
-    y.y += c.y;
-  }
-  if (b > 0) {
-    float2& y = sh.y[pad((kN - b) & (kM - 1))];
-    const float2 c = cmul(cB, make_float2(X.x, -X.y));
-    y.x += c.x;
-    y.y += c.y;
-  }
+// decode, one cluster of 2 CTAs per chunk.
+//
+// The inverse real FFT of X[0..N] (N = 32768, M = N/2) runs as two 16384-
+// point FFTs, CTA r transforming Y_r (z[2n + r] = IFFT_M(Y_r)[n]):
+//   Y_r[m] = cA(m) X[m] + cA(m+M) X[m+M] + cB(N-m) conj X[N-m] + cB(M-m) conj X[M-m]
+//   cA(b) = (1 + i W_L^-b) / 2,  cB(b) = (1 + i W_L^b) / 2, times W_N^-b / W_N^b for r = 1
+// (the real-IFFT pre-processing Z[k] = E + i W_L^-k O folded by the DIT
+// split).  The four bins {k, M-k, M+k, N-k} feed exactly Y_0 and Y_1 at m = k
+// and m = M-k, so chunk bins are owned by groups: CTA 0 owns the groups
+// k in [0, 4096) -- 32-bin blocks [0, 4096), [12288, 20480), [28672, 32768] --
+// and CTA 1 the groups k in [4096, 8192] -- blocks [4096, 12288), [20480, 28672)
+// (group 4096's bins 12288 and 28672 sit in CTA 0 and are read over DSMEM).
+//
+// Phase 1: thread t owns one 32-bin block; for every message, in worker
+// order, it adds weight_w * value of each non-zero slot of its block into its
+// own shared-memory entries: single writer, deterministic on every rank.
+// Phase 2: each CTA turns its groups into Y_0 and Y_1 values and stores the
+// peer's half over DSMEM (64 KB each way), then runs its inverse FFT.
+__device__ __forceinline__ uint32_t dec_block(uint32_t r, uint32_t t) {
+  if (r == 0) return t < 128 ? t : (t < 384 ? t + 256 : t + 512);
+  return t < 256 ? t + 128 : t + 384;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
+// cA / cB for both CTAs: wb = W_L^b, wn = W_N^b = wb^2
+__device__ __forceinline__ void coefs(float2 wb, float2 wn, float2& a0, float2& a1, float2& b0, float2& b1) {
+  a0 = make_float2(0.5f * (1.0f + wb.y), 0.5f * wb.x);
+  b0 = make_float2(0.5f * (1.0f - wb.y), 0.5f * wb.x);
+  a1 = cmulc(a0, wn);
+  b1 = cmul(b0, wn);
+}
+
+// Y_0 and Y_1 at m from X[m], X[m+M], X[N-m], X[M-m] with w = W_L^m, w2 = W_N^m.
+__device__ __forceinline__ void y_pair(float2 xm, float2 xmM, float2 xNm, float2 xMm, float2 w, float2 w2,
+                                       float2& y0, float2& y1) {
+  float2 a0, a1, b0, b1;
+  coefs(w, w2, a0, a1, b0, b1);
+  y0 = cmul(a0, xm);
+  y1 = cmul(a1, xm);
+  coefs(make_float2(w.y, -w.x), make_float2(-w2.x, -w2.y), a0, a1, b0, b1);      // b = m + M
+  y0 = cadd(y0, cmul(a0, xmM));
+  y1 = cadd(y1, cmul(a1, xmM));
+  coefs(make_float2(-w.x, w.y), conjf2(w2), a0, a1, b0, b1);                      // b = N - m
+  y0 = cadd(y0, cmul(b0, conjf2(xNm)));
+  y1 = cadd(y1, cmul(b1, conjf2(xNm)));
+  coefs(make_float2(-w.y, -w.x), make_float2(-w2.x, w2.y), a0, a1, b0, b1);       // b = M - m
+  y0 = cadd(y0, cmul(b0, conjf2(xMm)));
+  y1 = cadd(y1, cmul(b1, conjf2(xMm)));
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   DecodeShared& sh = *reinterpret_cast<DecodeShared*>(smem_raw);
-  const uint32_t r = blockIdx.x & 1u;
+  cg::cluster_group cluster = cg::this_cluster();
+  const uint32_t r = cluster.block_rank();
   const uint32_t chunk = a.first + blockIdx.x / 2;
   const ChunkInfo ci = a.chunks[chunk];
   const uint32_t tid = threadIdx.x;
@@ -725,100 +755,203 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
   }
   sh.t1024[tid] = a.t1024[tid];
   sh.t1024[tid + 512] = a.t1024[tid + 512];
-  {
-    float4* z = reinterpret_cast<float4*>(sh.y);
-    for (uint32_t e = tid; e < (kPadded + 64) / 2; e += kThreads) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  __syncthreads();
+  float2* acc = sh.x;
+  const uint32_t dbg = g_fused_dbg;
+  const uint32_t blk = dec_block(r, tid);                  // my 32-bin block
+  const bool binN = (r == 0 && tid == kThreads - 1);       // also owns bin N (local slot 16384)
+  float2* mine = acc + pad(32u * tid);                     // pad(32 t + j) = pad(32 t) + j
 
   if (a.spectrum) {
-    // dense spectrum input: four quarters, one bin per thread per step
-    const float2* X = a.spectrum + ci.bin_off;
-    for (uint32_t qq = 0; qq < 4; ++qq) {
-      const uint32_t lo = qq * (kN / 4), hi = (qq == 3) ? kBins : (qq + 1) * (kN / 4);
-      for (uint32_t b = lo + tid; b < hi; b += kThreads) {
-        float2 x = X[b];
-        if (b == 0 || b == kN) x.y = 0.f;
-        scatter_bin(sh, r, b, x, tw(sh.thi, sh.tlo, b));
-      }
-      __syncthreads();
-    }
+    // dense spectrum input (inverse_spectrum / debug hook)
+    const float2* X = a.spectrum + ci.bin_off + 32u * blk;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) mine[j] = X[j];
+    if (binN) acc[pad(kHalfBins)] = a.spectrum[ci.bin_off + kN];
   } else {
-    const int N = a.q.n_bits;
-    for (int w = 0; w < a.W; ++w) {
-      const uint8_t* seg = a.messages + (uint64_t)w * a.stride + ci.seg_off;
-      const uint32_t* bmg = reinterpret_cast<const uint32_t*>(seg + kSegHeader);
-      const uint32_t* cw = reinterpret_cast<const uint32_t*>(seg + ci.code_off);
-      // bitmap (slot order) + exclusive popcount prefix per word
-      uint32_t loc[5], local = 0;
-      const uint32_t w0 = 4 * tid, nw = (tid == kThreads - 1) ? 5u : 4u;
+    {
+      float4* z = reinterpret_cast<float4*>(acc);
+      for (uint32_t e = tid; e < (kPadded + 64) / 2; e += kThreads) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const uint32_t N = (uint32_t)a.q.n_bits;
+    FGC_TS(0);
+    for (int w0 = 0; w0 < a.W; w0 += kDecBatch) {
+      const int G = min(kDecBatch, a.W - w0);
+      // 1a. every bitmap word of the batch (thread t: blocks 2t, 2t+1), block code prefixes
+      uint32_t cnt2[kDecBatch][2];
 #pragma unroll
-      for (uint32_t k = 0; k < 5; ++k) {
-        loc[k] = 0;
-        if (k < nw) {
-          loc[k] = ballot_to_wire(__ldg(bmg + w0 + k));
-          local += __popc(loc[k]);
+      for (int i = 0; i < kDecBatch; ++i) {
+        cnt2[i][0] = cnt2[i][1] = 0u;
+        if (i < G) {
+          const uint32_t* bmg =
+              reinterpret_cast<const uint32_t*>(a.messages + (uint64_t)(w0 + i) * a.stride + ci.seg_off + kSegHeader);
+          const uint4 q4 = __ldg(reinterpret_cast<const uint4*>(bmg) + tid);
+          const uint4 nat = make_uint4(ballot_to_wire(q4.x), ballot_to_wire(q4.y), ballot_to_wire(q4.z),
+                                       ballot_to_wire(q4.w));
+          reinterpret_cast<uint4*>(sh.bm[i])[tid] = nat;
+          cnt2[i][0] = __popc(nat.x) + __popc(nat.y);
+          cnt2[i][1] = __popc(nat.z) + __popc(nat.w);
+          if (tid == 0) sh.bmN[i] = ballot_to_wire(__ldg(bmg + 2 * kThreads * 2)) & 3u;
         }
       }
-      uint32_t tot;
-      uint32_t base = block_exclusive_scan<kThreads>(local, sh.scan, tot);
+      uint4 tot;
+      const uint4 pre = block_exclusive_scan4<kThreads>(
+          make_uint4(cnt2[0][0] + cnt2[0][1], cnt2[1][0] + cnt2[1][1], cnt2[2][0] + cnt2[2][1],
+                     cnt2[3][0] + cnt2[3][1]), sh.scan, tot);
+      const uint32_t pr[4] = {pre.x, pre.y, pre.z, pre.w};
 #pragma unroll
-      for (uint32_t k = 0; k < 5; ++k) {
-        if (k < nw) {
-          sh.bm[w0 + k] = loc[k];
-          sh.pref[w0 + k] = base;
-          base += __popc(loc[k]);
+      for (int i = 0; i < kDecBatch; ++i) {
+        if (i < G) {
+          sh.pref[i][2 * tid] = pr[i];
+          sh.pref[i][2 * tid + 1] = pr[i] + cnt2[i][0];
         }
       }
       __syncthreads();
-      const float wt = a.wts.w[w];
-      for (uint32_t qq = 0; qq < 4; ++qq) {
-        const uint32_t nwq = (qq == 3 && tid == 0) ? 2u : 1u;
-        for (uint32_t e = 0; e < nwq; ++e) {
-          const uint32_t word = (e == 0) ? qq * 512u + tid : kBmWords - 1;
-          const uint32_t sw0 = sh.bm[word];
-          uint32_t sw = sw0;
-          if (!sw) continue;
-          const uint32_t pb = sh.pref[word];
-          const float2 wbase = tw(sh.thi, sh.tlo, 16u * word);
-          while (sw) {
-            const uint32_t pos = __ffs(sw) - 1;          // lowest set slot bit
-            const uint32_t jb = pos >> 1;
-            const uint32_t bits = (sw >> (2 * jb)) & 3u;
-            sw &= ~(3u << (2 * jb));
-            uint32_t rank = pb + __popc(sw0 & ((1u << (2 * jb)) - 1u));
-            float re = 0.f, im = 0.f;
-            if (bits & 1u) { re = decode_code(a.q, read_bits(cw, (uint64_t)rank * N, N)); ++rank; }
-            if (bits & 2u) im = decode_code(a.q, read_bits(cw, (uint64_t)rank * N, N));
-            const uint32_t b = word * 16u + jb;
-            if (b == 0 || b == kN) im = 0.f;
-            scatter_bin(sh, r, b, make_float2(re * wt, im * wt), cmul(wbase, sh.tlo[jb]));   // W_L^(16 word + jb)
-          }
+      if (w0 == 0) FGC_TS(7);
+      // 1b. my block's slots; the first code words of every message of the batch are loaded together
+      uint32_t wd[kDecBatch][3], idx[kDecBatch], win[kDecBatch][4], wbase[kDecBatch];
+      const uint32_t* cwp[kDecBatch];
+#pragma unroll
+      for (int i = 0; i < kDecBatch; ++i) {
+        wd[i][0] = wd[i][1] = wd[i][2] = 0u;
+        idx[i] = 0u;
+        wbase[i] = 0u;
+        cwp[i] = nullptr;
+        if (i < G) {
+          wd[i][0] = sh.bm[i][2 * blk];
+          wd[i][1] = sh.bm[i][2 * blk + 1];
+          if (binN) wd[i][2] = sh.bmN[i];
+          idx[i] = sh.pref[i][blk];
+          cwp[i] = reinterpret_cast<const uint32_t*>(a.messages + (uint64_t)(w0 + i) * a.stride + ci.seg_off +
+                                                     ci.code_off);
+          wbase[i] = (idx[i] * N) >> 5;
         }
-        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          win[i][q] = 0u;
+          if (i < G && (wd[i][0] | wd[i][1] | wd[i][2]) && wbase[i] + q < ci.code_cap)
+            win[i][q] = __ldg(cwp[i] + wbase[i] + q);
+        }
       }
+#pragma unroll
+      for (int i = 0; i < kDecBatch; ++i) {
+        if (i >= G) break;
+        const float wt = a.wts.w[w0 + i];
+        // codes are consumed in stream order: a 4-word window that slides by one word
+        uint32_t A = win[i][0], B = win[i][1], C = win[i][2], D = win[i][3];
+        uint32_t o = (idx[i] * N) & 31u, nxt = wbase[i] + 4u;
+        const uint32_t mask = (1u << N) - 1u;
+        auto run = [&](uint64_t m64, float* basef) {   // slot s of the block is float s of its entries
+          while (m64) {
+            const uint32_t pos = __ffsll((long long)m64) - 1;
+            m64 &= m64 - 1;
+            const uint32_t c = __funnelshift_r(A, B, o) & mask;
+            o += N;
+            if (o >= 32u) {
+              o -= 32u;
+              A = B; B = C; C = D;
+              D = nxt < ci.code_cap ? __ldg(cwp[i] + nxt) : 0u;
+              ++nxt;
+            }
+            // decode_code (quantizer.py:239-253) without branches
+            const bool neg = c > a.q.npos;
+            const uint32_t e = a.q.pbase + c - 1u - (neg ? a.q.npos : 0u);
+            const float v = __uint_as_float((e << a.q.shift) | (neg ? 0x80000000u : 0u));
+            basef[pos] += (c ? v : 0.0f) * wt;
+          }
+        };
+        run(((uint64_t)wd[i][1] << 32) | wd[i][0], reinterpret_cast<float*>(mine));
+        if (binN) run(wd[i][2], reinterpret_cast<float*>(acc + pad(kHalfBins)));
+      }
+      if (w0 == 0) FGC_TS(8);
+      __syncthreads();                                      // bm / pref reusable
+    }
+    FGC_TS(1);
+  }
+  cluster.sync();                                           // every X entry of the chunk is final
+  FGC_TS(2);
+
+  // ---- phase 2: my groups -> Y_0, Y_1 at m = k and m = M - k (registers)
+  const float2* peer = cluster.map_shared_rank(acc, r ^ 1);
+  float2 ys[8][4];                                          // {Y0[k], Y1[k], Y0[M-k], Y1[M-k]}
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t k = (r ? 4096u : 0u) + tid + 512u * i;
+    float2 xk, xMk, xkM, xNk;                               // X[k], X[M-k], X[k+M], X[N-k]
+    if (r == 0) {
+      xk = acc[pad(k)];
+      xMk = acc[pad(8192u - k)];
+      xkM = acc[pad(8192u + k)];
+      xNk = acc[pad(16384u - k)];
+    } else {
+      xk = acc[pad(k - 4096u)];
+      xkM = acc[pad(k + 4096u)];
+      if (k == 4096u) {                                     // bins 12288, 28672 live in CTA 0
+        xMk = peer[pad(4096u)];
+        xNk = peer[pad(12288u)];
+      } else {
+        xMk = acc[pad(12288u - k)];
+        xNk = acc[pad(20480u - k)];
+      }
+    }
+    if (k == 0) { xk.y = 0.f; xNk.y = 0.f; }                // imag of DC / Nyquist ignored
+    const float2 w = tw(sh.thi, sh.tlo, k);                 // W_L^k
+    const float2 w2 = cmul(w, w);                           // W_N^k
+    y_pair(xk, xkM, xNk, xMk, w, w2, ys[i][0], ys[i][1]);
+    // m' = M - k: X[m'] = X[M-k], X[m'+M] = X[N-k], X[N-m'] = X[M+k], X[M-m'] = X[k]
+    const float2 wp = make_float2(-w.y, -w.x);              // W_L^(M-k) = -i conj w
+    const float2 w2p = make_float2(-w2.x, w2.y);            // W_N^(M-k) = -conj w2
+    y_pair(xMk, xNk, xkM, xk, wp, w2p, ys[i][2], ys[i][3]);
+  }
+  // CTA 1's extra group k = 8192 (m = M - m = 8192): bins 8192 (slot 4096) and 24576 (slot 12288)
+  float2 y8192_0 = make_float2(0.f, 0.f), y8192_1 = make_float2(0.f, 0.f);
+  if (r == 1 && tid == 0) {
+    const float2 x8 = acc[pad(4096u)], x24 = acc[pad(12288u)];
+    const float2 w = tw(sh.thi, sh.tlo, 8192u), w2 = cmul(w, w);
+    y_pair(x8, x24, x24, x8, w, w2, y8192_0, y8192_1);
+  }
+  FGC_TS(3);
+  cluster.sync();                                           // all X reads done (both CTAs)
+  FGC_TS(4);
+  float2* yo = acc;                                         // Y_r in natural m order (FFT input)
+  float2* yp = cluster.map_shared_rank(acc, r ^ 1);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t k = (r ? 4096u : 0u) + tid + 512u * i;
+    yo[pad(k)] = r ? ys[i][1] : ys[i][0];
+    yp[pad(k)] = r ? ys[i][0] : ys[i][1];
+    if (k != 0) {
+      yo[pad(kHalfBins - k)] = r ? ys[i][3] : ys[i][2];
+      yp[pad(kHalfBins - k)] = r ? ys[i][2] : ys[i][3];
     }
   }
+  if (r == 1 && tid == 0) {
+    yo[pad(8192u)] = y8192_1;
+    yp[pad(8192u)] = y8192_0;
+  }
+  cluster.sync();                                           // Y_r complete in both CTAs
+  FGC_TS(9);
 
   // inverse 16384-point FFT of Y_r, natural-order output
   float2 v[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = sh.y[pad(tid + 512u * j)];
+  for (int j = 0; j < 32; ++j) v[j] = acc[pad(tid + 512u * j)];
   __syncthreads();
-  fft_pass12<true>(v, sh.y, sh.t1024);
+  fft_pass12<true>(v, sh.x, sh.t1024);
   __syncthreads();
+  FGC_TS(5);
   const float scale = 1.0f / (float)kN;
   float* out = a.out + ci.in_off;
   for (uint32_t c = 0; c < 2; ++c) {
     const uint32_t k = tid + 512u * c;
     float2 o[16];
-    fft_pass3<true>(k, sh.y, o, sh.thi, sh.tlo);
+    fft_pass3<true>(k, sh.x, o, sh.thi, sh.tlo);
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
       const uint32_t p = k + 1024u * m;
       *reinterpret_cast<float2*>(out + 4ull * p + 2 * r) = make_float2(o[m].x * scale, o[m].y * scale);
     }
   }
+  FGC_TS(6);
 }
 
 template <class K>
