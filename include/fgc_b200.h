@@ -274,9 +274,16 @@ fgc_status fgc_allgather(void* comm, const uint8_t* send, uint8_t* recv, uint64_
 /* Uncompressed baseline: in-place float32 sum allreduce. */
 fgc_status fgc_allreduce_sum_f32(void* comm, float* data, uint64_t count, void* stream);
 
-/* One fused step of the compressed average for this rank:
- * compress(grad) -> allgather -> decode_average(weights) -> out.
- * gathered must hold nranks * message_bytes.  comm may be NULL for W=1. */
+/* One step of the compressed average for this rank (simulator.py:520-547):
+ * compress(grad) -> allgather -> decode_average(weights) -> out, pipelined
+ * in pieces of consecutive chunks (whole waves of the fused kernels;
+ * FGC_PIPELINE_WAVES per piece; default 0 = one piece): piece i
+ * is allgathered on an internal high-priority stream while piece i+1
+ * compresses, and decoded when its exchange completes.  gathered must hold
+ * nranks * message_bytes; its layout is piece-major (piece i of every rank
+ * contiguous), i.e. internal.  comm may be NULL for W=1.  Work is ordered
+ * after prior work on `stream` and everything it launches is joined back
+ * into `stream`. */
 fgc_status fgc_allgather_average(fgc_plan* plan, void* comm, int nranks, const void* grad,
                                  int dtype, const double* weights, uint8_t* message,
                                  uint8_t* gathered, float* out, uint32_t* flags, void* stream);

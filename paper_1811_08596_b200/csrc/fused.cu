@@ -50,6 +50,7 @@ struct FusedTables {
   float2* thi = nullptr;     // W_65536^(256 h), h < 256
   float2* tlo = nullptr;     // W_65536^l, l < 256
   float2* t1024 = nullptr;   // W_1024^m, m < 1024
+  uint32_t wave = 74;        // clusters resident at once (SMs / 2): the L2 prefetch distance
 };
 
 __device__ uint32_t g_fused_dbg = 0;                  // instrumentation knobs (0 in production)
@@ -156,6 +157,8 @@ struct CompressArgs {
   uint32_t* fb;          // per-chunk fallback flag (indexed by chunk id)
   float2* fb_spec;       // chunk-major spectrum scratch for fallback chunks
   float2* dbg_spec;      // debug hook: write the spectrum and stop
+  uint32_t count;        // chunks in this launch
+  uint32_t ahead;        // L2 prefetch distance in chunks (one wave)
 };
 
 struct __align__(16) CompressShared {
@@ -323,6 +326,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   }
 
   FGC_TS(1);
+  if (tid == 0 && blockIdx.x / 2 + a.ahead < a.count) {
+    // the chunk the next wave runs here: its HBM read overlaps this wave's compute
+    const ChunkInfo cn = a.chunks[chunk + a.ahead];
+    const uint32_t half_bytes = (uint32_t)(kL / 2 * sizeof(T));
+    const char* base = reinterpret_cast<const char*>(static_cast<const T*>(a.grad) + cn.in_off) + (uint64_t)r * half_bytes;
+    for (uint32_t off = 0; off < half_bytes; off += 32768u)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off), "r"(32768u) : "memory");
+  }
   // ---- 2. 16384-point FFT: passes 1, 2 (transposes in smem), pass 3 on two columns
   fft_pass12<false>(v, sh.buf, sh.t1024);
   FGC_TS(2);
@@ -678,6 +689,8 @@ struct DecodeArgs {
   const float2* tlo;
   const float2* t1024;
   const float2* spectrum;     // dense-spectrum mode (debug hook), else null
+  uint32_t count;             // chunks in this launch
+  uint32_t ahead;             // L2 prefetch distance in chunks (one wave)
 };
 
 constexpr int kDecBatch = 4;                           // messages per block scan in the decode
@@ -760,6 +773,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   const uint32_t blk = dec_block(r, tid);                  // my 32-bin block
   const bool binN = (r == 0 && tid == kThreads - 1);       // also owns bin N (local slot 16384)
   float2* mine = acc + pad(32u * tid);                     // pad(32 t + j) = pad(32 t) + j
+  if (!a.spectrum && tid < (uint32_t)a.W && blockIdx.x / 2 + a.ahead < a.count) {
+    // message segments of the chunk the next wave decodes here (CTA r: half of each)
+    const ChunkInfo cn = a.chunks[chunk + a.ahead];
+    const uint32_t seg = (uint32_t)(cn.code_off + 4ull * ((cn.code_cap + 3u) & ~3u));
+    const uint32_t half = ((seg / 2) + 15u) & ~15u;
+    const uint32_t lo = r ? half : 0u, bytes = r ? seg - half : half;
+    if (bytes)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                   ::"l"(a.messages + (uint64_t)tid * a.stride + cn.seg_off + lo), "r"(bytes) : "memory");
+  }
 
   if (a.spectrum) {
     // dense spectrum input (inverse_spectrum / debug hook)
@@ -986,6 +1009,12 @@ fgc_status fused_tables_init(FusedTables** t, cudaStream_t s) {
     fused_tables_free(ft);
     return cuda_check(e, "cudaMalloc");
   }
+  {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    ft->wave = (uint32_t)(sms / 2);
+  }
   k_init_tables<<<1, 1024, 0, s>>>(ft->thi, ft->tlo, ft->t1024);
   FGC_LAUNCHED(1);
   static bool attrs = false;
@@ -1019,7 +1048,7 @@ static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_
                                        const QuantParams& q, uint8_t* message, uint32_t* flags, uint32_t* fb,
                                        float2* fb_spec, float2* dbg, cudaStream_t s) {
   if (!count) return FGC_OK;
-  CompressArgs a{d_chunks, first, grad, q, message, flags, t->thi, t->tlo, t->t1024, fb, fb_spec, dbg};
+  CompressArgs a{d_chunks, first, grad, q, message, flags, t->thi, t->tlo, t->t1024, fb, fb_spec, dbg, count, t->wave};
   const size_t smem = sizeof(CompressShared);
   const dim3 grid(2 * count), block(kThreads);
   const bool f64 = dtype == FGC_DTYPE_F64, h = half_pass != 0;
@@ -1061,7 +1090,7 @@ fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, 
                                const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
                                const QuantParams& q, float* out, cudaStream_t s) {
   if (!count) return FGC_OK;
-  DecodeArgs a{d_chunks, first, messages, W, stride, wts, q, out, t->thi, t->tlo, t->t1024, nullptr};
+  DecodeArgs a{d_chunks, first, messages, W, stride, wts, q, out, t->thi, t->tlo, t->t1024, nullptr, count, t->wave};
   k_fused_decode<<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
   FGC_LAUNCHED(1);
   return FGC_OK;

@@ -50,6 +50,9 @@ struct fgc_plan {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   FusedTables* fused = nullptr;
   uint32_t fused_first = 0, fused_count = 0;     // chunk range taken by fused kernels
+  // pipelined allgather-average: exchange stream + per-piece events (created on first use)
+  cudaStream_t xstream = nullptr;
+  std::vector<cudaEvent_t> ev_comp, ev_gath;
 };
 
 static QuantParams make_qparams(const fgc_codec_desc& d) {
@@ -243,6 +246,9 @@ extern "C" void fgc_plan_destroy(fgc_plan* p) {
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->side) cudaStreamDestroy(p->side);
+  for (cudaEvent_t e : p->ev_comp) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_gath) cudaEventDestroy(e);
+  if (p->xstream) cudaStreamDestroy(p->xstream);
   delete p;
 }
 
@@ -296,35 +302,42 @@ static fgc_status check_mode(const fgc_plan* p) {
   return FGC_OK;
 }
 
-extern "C" fgc_status fgc_compress(fgc_plan* p, const void* grad, int dtype, uint8_t* message, uint32_t* flags,
-                                   void* stream) {
-  if (!p || !grad || !message || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
-  FGC_TRY(check_mode(p));
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // generic classes (tails) run on the side stream, overlapped with the fused kernel
-  const bool fork = p->fused_count && p->classes.size() > 1;
+// Compress the fused chunks [f0, f0 + fc) and, when `generic`, every generic
+// (tail) class -- those on the high-priority side stream, joined back into s.
+static fgc_status compress_range(fgc_plan* p, const void* grad, int dtype, uint8_t* message, uint32_t* flags,
+                                 cudaStream_t s, uint32_t f0, uint32_t fc, bool generic) {
+  const bool fork = generic && fc && p->classes.size() > 1;
   cudaStream_t g = fork ? p->side : s;
   if (fork) {
     FGC_CUDA(cudaEventRecord(p->ev_fork, s));
     FGC_CUDA(cudaStreamWaitEvent(g, p->ev_fork, 0));
   }
-  FGC_TRY(forward_generic(p, grad, dtype, p->d_spec, flags, g, false));
-  for (RealClass& rc : p->classes) {
-    if (rc.fused) continue;
-    FGC_TRY(launch_select_pack(p->d_chunks, rc.first, rc.count, p->d_spec, 0, p->q, message, nullptr, flags, g));
+  if (generic) {
+    FGC_TRY(forward_generic(p, grad, dtype, p->d_spec, flags, g, false));
+    for (RealClass& rc : p->classes) {
+      if (rc.fused) continue;
+      FGC_TRY(launch_select_pack(p->d_chunks, rc.first, rc.count, p->d_spec, 0, p->q, message, nullptr, flags, g));
+    }
   }
-  if (p->fused_count) {
-    FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, p->fused_first, p->fused_count, grad, dtype,
-                                  p->desc.half_pass, p->q, message, flags, p->d_fb, p->d_spec, s));
+  if (fc) {
+    FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, f0, fc, grad, dtype, p->desc.half_pass, p->q, message,
+                                  flags, p->d_fb, p->d_spec, s));
     // degenerate chunks the fused select handed back (flag set, spectrum in d_spec)
-    FGC_TRY(launch_select_pack(p->d_chunks, p->fused_first, p->fused_count, p->d_spec, 0, p->q, message, nullptr,
-                               flags, s, p->d_fb));
+    FGC_TRY(launch_select_pack(p->d_chunks, f0, fc, p->d_spec, 0, p->q, message, nullptr, flags, s, p->d_fb));
   }
   if (fork) {
     FGC_CUDA(cudaEventRecord(p->ev_join, g));
     FGC_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
   }
   return FGC_OK;
+}
+
+extern "C" fgc_status fgc_compress(fgc_plan* p, const void* grad, int dtype, uint8_t* message, uint32_t* flags,
+                                   void* stream) {
+  if (!p || !grad || !message || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_mode(p));
+  return compress_range(p, grad, dtype, message, flags, static_cast<cudaStream_t>(stream), p->fused_first,
+                        p->fused_count, true);
 }
 
 extern "C" fgc_status fgc_encode_spectrum(fgc_plan* p, const void* spectrum, uint8_t* message, uint8_t* kept_mask,
@@ -364,32 +377,39 @@ static fgc_status inverse_generic(fgc_plan* p, const float2* spectrum, float* ou
   return FGC_OK;
 }
 
-extern "C" fgc_status fgc_decode_average(fgc_plan* p, const uint8_t* messages, int W, uint64_t stride,
-                                         const double* weights, float* out, void* stream) {
-  if (!p || !messages || !out) { set_error("null argument"); return FGC_ERR_INVALID; }
-  Weights w;
-  FGC_TRY(fill_weights(weights, W, w));
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const bool fork = p->fused_count && p->classes.size() > 1;
+// Decode-average the fused chunks [f0, f0 + fc) (and the generic classes when
+// `generic`).  Message w's chunk c lives at messages + w * stride + seg_off(c).
+static fgc_status decode_range(fgc_plan* p, const uint8_t* messages, int W, uint64_t stride, const Weights& w,
+                               float* out, cudaStream_t s, uint32_t f0, uint32_t fc, bool generic) {
+  const bool fork = generic && fc && p->classes.size() > 1;
   cudaStream_t g = fork ? p->side : s;
   if (fork) {
     FGC_CUDA(cudaEventRecord(p->ev_fork, s));
     FGC_CUDA(cudaStreamWaitEvent(g, p->ev_fork, 0));
   }
-  for (RealClass& rc : p->classes) {
-    if (rc.fused) continue;
-    FGC_TRY(launch_decode_accumulate(p->d_chunks, rc.first, rc.count, messages, W, stride, w, p->q, p->d_spec,
-                                     p->max_slots, g));
+  if (generic) {
+    for (RealClass& rc : p->classes) {
+      if (rc.fused) continue;
+      FGC_TRY(launch_decode_accumulate(p->d_chunks, rc.first, rc.count, messages, W, stride, w, p->q, p->d_spec,
+                                       p->max_slots, g));
+    }
+    FGC_TRY(inverse_generic(p, p->d_spec, out, g));
   }
-  FGC_TRY(inverse_generic(p, p->d_spec, out, g));
-  if (p->fused_count)
-    FGC_TRY(launch_fused_decode(p->fused, p->d_chunks, p->fused_first, p->fused_count, messages, W, stride, w, p->q,
-                                out, s));
+  if (fc) FGC_TRY(launch_fused_decode(p->fused, p->d_chunks, f0, fc, messages, W, stride, w, p->q, out, s));
   if (fork) {
     FGC_CUDA(cudaEventRecord(p->ev_join, g));
     FGC_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
   }
   return FGC_OK;
+}
+
+extern "C" fgc_status fgc_decode_average(fgc_plan* p, const uint8_t* messages, int W, uint64_t stride,
+                                         const double* weights, float* out, void* stream) {
+  if (!p || !messages || !out) { set_error("null argument"); return FGC_ERR_INVALID; }
+  Weights w;
+  FGC_TRY(fill_weights(weights, W, w));
+  return decode_range(p, messages, W, stride, w, out, static_cast<cudaStream_t>(stream), p->fused_first,
+                      p->fused_count, true);
 }
 
 extern "C" fgc_status fgc_decode_spectrum(fgc_plan* p, const uint8_t* messages, int W, uint64_t stride,
@@ -555,13 +575,64 @@ extern "C" fgc_status fgc_allgather_average(fgc_plan* p, void* comm, int nranks,
                                             const double* weights, uint8_t* message, uint8_t* gathered, float* out,
                                             uint32_t* flags, void* stream) {
   if (!p || !grad || !message || !out || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
-  FGC_TRY(fgc_compress(p, grad, dtype, message, flags, stream));
-  if (nranks > 1) {
-    if (!comm || !gathered) { set_error("multi-rank average needs a communicator and a gather buffer"); return FGC_ERR_INVALID; }
-    FGC_TRY(fgc_allgather(comm, message, gathered, p->msg_bytes, stream));
-    return fgc_decode_average(p, gathered, nranks, p->msg_bytes, weights, out, stream);
+  if (nranks <= 1) {
+    FGC_TRY(fgc_compress(p, grad, dtype, message, flags, stream));
+    return fgc_decode_average(p, message, 1, p->msg_bytes, weights, out, stream);
   }
-  return fgc_decode_average(p, message, 1, p->msg_bytes, weights, out, stream);
+  if (!comm || !gathered) { set_error("multi-rank average needs a communicator and a gather buffer"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_mode(p));
+  Weights w;
+  FGC_TRY(fill_weights(weights, nranks, w));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // Pipeline in P pieces of consecutive chunks (their segments are contiguous):
+  // piece i is allgathered on the exchange stream while piece i+1 compresses,
+  // and decoded once its exchange is done.  The gather buffer holds piece i of
+  // all ranks contiguously at W * seg_off(first chunk of i).
+  // Pieces are whole waves of fused clusters (one 2-CTA cluster per 2 SMs), so
+  // splitting the launches adds no partial waves; a short remainder joins the
+  // last piece.  FGC_PIPELINE_WAVES sets the waves per piece (default 0 = one piece:
+  // measured on 4 B200s, NCCL's allgather kernels competing for SMs cost more
+  // than the overlap gains).
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint32_t wpp = 0;
+  if (const char* e = getenv("FGC_PIPELINE_WAVES")) wpp = (uint32_t)std::max(0, atoi(e));
+  const uint32_t per = std::max(1u, wpp * (uint32_t)(sms / 2));
+  uint32_t P = wpp ? std::max(1u, p->fused_count / per) : 1u;
+  std::vector<uint32_t> f(P + 1);
+  for (uint32_t i = 0; i < P; ++i) f[i] = p->fused_first + i * per;
+  f[P] = p->fused_first + p->fused_count;                // the remainder (< 2 pieces) joins the last
+  if (!p->xstream) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    FGC_CUDA(cudaStreamCreateWithPriority(&p->xstream, cudaStreamNonBlocking, greatest));
+  }
+  while (p->ev_comp.size() < P) {
+    cudaEvent_t a, b;
+    FGC_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    FGC_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    p->ev_comp.push_back(a);
+    p->ev_gath.push_back(b);
+  }
+  // the generic (tail) chunks ride with the last piece
+  auto piece_lo = [&](uint32_t i) -> uint64_t { return i == 0 ? 0 : p->seg_off[f[i]]; };
+  auto piece_hi = [&](uint32_t i) -> uint64_t { return i + 1 == P ? p->msg_bytes : p->seg_off[f[i + 1]]; };
+  for (uint32_t i = 0; i < P; ++i) {
+    FGC_TRY(compress_range(p, grad, dtype, message, flags, s, f[i], f[i + 1] - f[i], i + 1 == P));
+    FGC_CUDA(cudaEventRecord(p->ev_comp[i], s));
+    FGC_CUDA(cudaStreamWaitEvent(p->xstream, p->ev_comp[i], 0));
+    const uint64_t lo = piece_lo(i), bytes = piece_hi(i) - lo;
+    FGC_TRY(fgc_allgather(comm, message + lo, gathered + (uint64_t)nranks * lo, bytes, p->xstream));
+    FGC_CUDA(cudaEventRecord(p->ev_gath[i], p->xstream));
+  }
+  for (uint32_t i = 0; i < P; ++i) {
+    FGC_CUDA(cudaStreamWaitEvent(s, p->ev_gath[i], 0));
+    const uint64_t lo = piece_lo(i), bytes = piece_hi(i) - lo;
+    FGC_TRY(decode_range(p, gathered + (uint64_t)nranks * lo - lo, nranks, bytes, w, out, s, f[i], f[i + 1] - f[i],
+                         i + 1 == P));
+  }
+  return FGC_OK;
 }
 
 extern "C" const char* fgc_last_error(void) { return g_last_error.c_str(); }

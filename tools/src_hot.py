@@ -31,3 +31,7 @@ tot_s = sum(v[1] for v in agg.values()) or 1
 print(f"total warp-instr {tot_i:.3e}  stall samples {tot_s:.0f}")
 for (f, ln), (ie, ws, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
     print(f"{f:16s}{ln:5d} instr {ie/tot_i:6.1%} stall {ws/tot_s:6.1%}  {src}")
+if len(sys.argv) > 3 and sys.argv[3] == "stall":
+    print("--- by stall samples")
+    for (f, ln), (ie, ws, src) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+        print(f"{f:16s}{ln:5d} instr {ie/tot_i:6.1%} stall {ws/tot_s:6.1%}  {src}")
