@@ -288,6 +288,28 @@ fgc_status fgc_allgather_average(fgc_plan* plan, void* comm, int nranks, const v
                                  int dtype, const double* weights, uint8_t* message,
                                  uint8_t* gathered, float* out, uint32_t* flags, void* stream);
 
+/* ---- peer-memory exchange (copy engines over NVLink, CUDA IPC) ---------- */
+/* The allgather of simulator.py:529-535 without collective kernels: each
+ * rank pushes its message pieces into every peer's gather buffer with
+ * peer-to-peer copies and signals them with stream memory operations, so
+ * the exchange overlaps the codec kernels without taking SMs.  Setup:
+ * create on every rank, exchange the 128-byte handles (e.g. through
+ * torch.distributed), open with all ranks' handles (rank-major). */
+typedef struct fgc_exchange fgc_exchange;
+fgc_status fgc_exchange_create(int nranks, int rank, uint64_t message_bytes, fgc_exchange** out);
+fgc_status fgc_exchange_handles(fgc_exchange* x, uint8_t handles_out[128]);
+fgc_status fgc_exchange_open(fgc_exchange* x, const uint8_t* all_handles /* nranks * 128 */);
+void       fgc_exchange_destroy(fgc_exchange* x);   /* all ranks: after a barrier */
+/* This rank's message slot / the gather buffer of step parity `parity`. */
+fgc_status fgc_exchange_message(fgc_exchange* x, int parity, uint8_t** message, uint8_t** gathered);
+/* One averaging step over the exchange (same result as
+ * fgc_allgather_average): compress into this rank's slot piece by piece,
+ * push each piece to every peer as soon as it is compressed, decode each
+ * piece once every peer's copy of it has landed.  Steps alternate between
+ * two gather buffers; every rank must call it the same number of times. */
+fgc_status fgc_exchange_average(fgc_plan* plan, fgc_exchange* x, const void* grad, int dtype,
+                                const double* weights, float* out, uint32_t* flags, void* stream);
+
 /* ---- misc -------------------------------------------------------------- */
 const char* fgc_last_error(void);   /* thread-local message of the last failure */
 int         fgc_version(void);      /* 0xMMmmpp                                  */

@@ -18,6 +18,6 @@ from .spectral import (Spectrum, SparsificationSpec, dft_forward, dft_inverse, t
 from .packer import PackedSparse, pack, unpack, prefix_sum, bitmap_to_bytes, bitmap_from_bytes
 from .codec import (CodecConfig, ChunkPayload, CompressedMessage, compress, decompress, reconstruct,
                     reconstruct_rows, serialize, deserialize, calibrate, compression_ratio)
-from .comm import GradientAverager, NcclComm, allgather_average, message_layout, shard_weights
+from .comm import GradientAverager, NcclComm, PeerExchange, allgather_average, message_layout, shard_weights
 
 __version__ = "0.1.0"

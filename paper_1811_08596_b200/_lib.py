@@ -92,6 +92,12 @@ _SIGS = {
     "fgc_allgather": (I32, [P, P, P, U64, P]),
     "fgc_allreduce_sum_f32": (I32, [P, P, U64, P]),
     "fgc_allgather_average": (I32, [P, P, I32, P, I32, P, P, P, P, P, P]),
+    "fgc_exchange_create": (I32, [I32, I32, U64, C.POINTER(P)]),
+    "fgc_exchange_handles": (I32, [P, P]),
+    "fgc_exchange_open": (I32, [P, P]),
+    "fgc_exchange_destroy": (None, [P]),
+    "fgc_exchange_message": (I32, [P, I32, C.POINTER(P), C.POINTER(P)]),
+    "fgc_exchange_average": (I32, [P, P, P, I32, P, P, P, P]),
     "fgc_last_error": (C.c_char_p, []),
     "fgc_version": (I32, []),
     "fgc_kernel_launches": (U64, []),

@@ -27,7 +27,7 @@ from . import _device as D
 from . import _lib
 from .codec import CodecConfig, _desc, get_plan
 
-__all__ = ["message_layout", "shard_weights", "NcclComm", "GradientAverager", "allgather_average"]
+__all__ = ["message_layout", "shard_weights", "NcclComm", "PeerExchange", "GradientAverager", "allgather_average"]
 
 
 def message_layout(n: int, config: CodecConfig) -> tuple[int, int, np.ndarray]:
@@ -56,6 +56,7 @@ class NcclComm:
 
     def __init__(self, group=None):
         import torch.distributed as dist
+        self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         uid = np.zeros(128, dtype=np.uint8)
@@ -82,12 +83,48 @@ class NcclComm:
             self.handle = None
 
 
+class PeerExchange:
+    """Double-buffered gather buffers shared with every peer through CUDA IPC:
+    the copy engines move each rank's message pieces over NVLink while the
+    codec kernels run (fgc_exchange_*; no collective kernels on the SMs).
+    Handles are swapped through torch.distributed on ``group``."""
+
+    def __init__(self, message_bytes: int, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        D.require_cuda()
+        self.rank, self.world = rank, world
+        h = C.c_void_p()
+        _lib.check(_lib.lib.fgc_exchange_create(world, rank, message_bytes, C.byref(h)))
+        self.handle = h
+        mine = np.zeros(128, dtype=np.uint8)
+        _lib.check(_lib.lib.fgc_exchange_handles(h, mine.ctypes.data))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine.tobytes(), group=group)
+        buf = np.frombuffer(b"".join(allh), dtype=np.uint8).copy()
+        _lib.check(_lib.lib.fgc_exchange_open(h, buf.ctypes.data))
+        dist.barrier(group)
+        self._group = group
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            import torch.distributed as dist
+            torch.cuda.synchronize()
+            dist.barrier(self._group)          # no peer still reads our buffers
+            _lib.lib.fgc_exchange_destroy(self.handle)
+            self.handle = None
+
+
 class GradientAverager:
     """Persistent buffers + plan for repeated compressed averaging of an
     n-element gradient: the per-step call allocates nothing and launches
-    compress -> allgather -> decode-average on the current stream."""
+    compress -> exchange -> decode-average on the current stream.
 
-    def __init__(self, n: int, config: CodecConfig, weights, comm: NcclComm | None = None):
+    transport "peer" (default; FGC_TRANSPORT overrides): pieces of the
+    message move by peer-to-peer copies as soon as they are compressed and
+    are decoded as they land (PeerExchange).  "nccl": one ncclAllGather."""
+
+    def __init__(self, n: int, config: CodecConfig, weights, comm: NcclComm | None = None,
+                 transport: str | None = None):
         if config.sparsification.mode != "count":
             raise NotImplementedError("energy-mode selection is not implemented on the GPU")
         dev = D.require_cuda()
@@ -107,6 +144,18 @@ class GradientAverager:
                          if self.world > 1 else self.message)
         self.out = torch.empty(self.n, dtype=torch.float32, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        import os
+        self.transport = transport or os.environ.get("FGC_TRANSPORT", "peer")
+        if self.transport not in ("peer", "nccl"):
+            raise ValueError(f"unknown transport {self.transport!r}")
+        self.exchange = None
+        if self.world > 1 and self.transport == "peer":
+            self.exchange = PeerExchange(self.plan.message_bytes, comm.rank, comm.world, comm.group)
+
+    def close(self) -> None:
+        if self.exchange is not None:
+            self.exchange.close()
+            self.exchange = None
 
     def step(self, grad: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """Average this rank's device gradient with every other rank's."""
@@ -116,6 +165,11 @@ class GradientAverager:
         if grad.dtype not in (torch.float32, torch.float64):
             raise ValueError("gradient must be float32 or float64")
         dst = self.out if out is None else out
+        if self.exchange is not None:
+            _lib.check(_lib.lib.fgc_exchange_average(self.plan.handle, self.exchange.handle, grad.data_ptr(), code,
+                                                     self.weights.ctypes.data, dst.data_ptr(), self.flags.data_ptr(),
+                                                     D.stream()))
+            return dst
         comm = None if self.comm is None else self.comm.handle
         _lib.check(_lib.lib.fgc_allgather_average(self.plan.handle, comm, self.world, grad.data_ptr(), code,
                                                   self.weights.ctypes.data, self.message.data_ptr(),
@@ -136,6 +190,9 @@ def allgather_average(local_grad, config: CodecConfig, weights, comm: NcclComm |
     returns ``sum_w weights[w] * decompress(compress(grad_w))`` as float64."""
     t, code = D.as_signal(local_grad)
     avg = GradientAverager(t.numel(), config, weights, comm)
-    out = avg.step(t if t.dtype in (torch.float32, torch.float64) else t.float())
-    avg.check()
-    return out.double().cpu().numpy()
+    try:
+        out = avg.step(t if t.dtype in (torch.float32, torch.float64) else t.float())
+        avg.check()
+        return out.double().cpu().numpy()
+    finally:
+        avg.close()

@@ -113,7 +113,7 @@ template <typename CT>
 __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* chunks, uint32_t first, Coeffs<CT> coeffs,
                                                              int exact_only, QuantParams q, uint8_t* message,
                                                              uint8_t* kept_mask, uint32_t* flags,
-                                                             const uint32_t* only_if) {
+                                                             const uint32_t* only_if, PieceCounter pc) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SelectShared& sh = *reinterpret_cast<SelectShared*>(smem_raw);
   if (only_if && only_if[first + blockIdx.x] == 0u) return;
@@ -366,6 +366,11 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
   for (uint32_t w = used + tid; w < cap_padded; w += kSelThreads) codes[w] = 0;
   // zero the bitmap tail words beyond the last tile (none: tiles cover bins)
   if (overflow) atomicOr(flags, FGC_FLAG_CAPACITY);
+  if (pc.cnt) {                                  // segment complete: count it for the exchange
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(&pc.cnt[(first + blockIdx.x - pc.first) / pc.per], 1u);
+  }
 }
 
 // ------------------------------------------------------------- decode + accumulate
@@ -428,7 +433,7 @@ __global__ void __launch_bounds__(kDecThreads) k_decode_accumulate(const ChunkIn
 
 fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_t count, const void* spectrum,
                               int coeff_f64, const QuantParams& q, uint8_t* message, uint8_t* kept_mask,
-                              uint32_t* flags, cudaStream_t s, const uint32_t* only_if) {
+                              uint32_t* flags, cudaStream_t s, const uint32_t* only_if, PieceCounter pc) {
   if (!count) return FGC_OK;
   static bool attr = false;
   const size_t smem = sizeof(SelectShared);
@@ -440,11 +445,11 @@ fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_
   if (coeff_f64) {
     Coeffs<double2> c{static_cast<const double2*>(spectrum)};
     k_select_pack<double2><<<count, kSelThreads, smem, s>>>(d_chunks, first, c, 1, q, message, kept_mask, flags,
-                                                            only_if);
+                                                            only_if, pc);
   } else {
     Coeffs<float2> c{static_cast<const float2*>(spectrum)};
     k_select_pack<float2><<<count, kSelThreads, smem, s>>>(d_chunks, first, c, 0, q, message, kept_mask, flags,
-                                                           only_if);
+                                                           only_if, pc);
   }
   FGC_LAUNCHED(1);
   return FGC_OK;

@@ -138,9 +138,25 @@ fgc_status real_inverse(RealClassT<R>& rc, const ChunkInfo* d_chunks, const type
 // Select (count mode) + quantize + pack from a chunk-major spectrum.
 // Chunks [first, first+count).  coeff_f64: spectrum is double2.
 // only_if (may be null): skip chunk c unless only_if[c] != 0.
+// Per-piece completion counters for the peer exchange: chunk c adds one to
+// cnt[(c - first) / per] once its message segment is globally visible.
+struct PieceCounter {
+  uint32_t* cnt = nullptr;
+  uint32_t first = 0, per = 1;
+};
+
+// Decode-side wait of the peer exchange: before reading chunk c, every peer
+// b != me must have set flags[b * stride + (c - first) / per] >= target.
+struct PieceWait {
+  const uint32_t* flags = nullptr;
+  uint32_t stride = 0, first = 0, per = 1, target = 0;
+  int nranks = 0, me = 0;
+};
+
 fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_t count, const void* spectrum,
                               int coeff_f64, const QuantParams& q, uint8_t* message, uint8_t* kept_mask,
-                              uint32_t* flags, cudaStream_t s, const uint32_t* only_if = nullptr);
+                              uint32_t* flags, cudaStream_t s, const uint32_t* only_if = nullptr,
+                              PieceCounter pc = PieceCounter());
 
 // Decode + weighted accumulate of W messages into a chunk-major spectrum.
 struct Weights {
@@ -175,15 +191,32 @@ void fused_tables_free(FusedTables* t);
 // whose spectrum was written to fb_spec).
 fgc_status launch_fused_compress(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                  const void* grad, int dtype, int half_pass, const QuantParams& q, uint8_t* message,
-                                 uint32_t* flags, uint32_t* fb, float2* fb_spec, cudaStream_t s);
+                                 uint32_t* flags, uint32_t* fb, float2* fb_spec, cudaStream_t s,
+                                 PieceCounter pc = PieceCounter());
 fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
-                               const QuantParams& q, float* out, cudaStream_t s);
+                               const QuantParams& q, float* out, cudaStream_t s, PieceWait pw = PieceWait());
 // Debug hooks: the fused kernels' own forward coefficients / inverse.
 fgc_status launch_fused_spectrum(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                  const void* grad, int dtype, int half_pass, float2* spectrum, uint32_t* flags,
                                  cudaStream_t s);
 fgc_status launch_fused_inverse(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                 const float2* spectrum, float* out, cudaStream_t s);
+
+// Peer exchange internals (xchg.cu).
+fgc_status exchange_publish_event(fgc_exchange* x, int k, uint64_t lo, uint64_t bytes, cudaEvent_t ready,
+                                  uint32_t value);
+fgc_status exchange_publish_piece(fgc_exchange* x, int k, uint32_t i, uint64_t lo, uint64_t bytes,
+                                  uint32_t count_target, uint32_t value);
+fgc_status exchange_wait(fgc_exchange* x, cudaStream_t s, int fi, uint32_t value);
+PieceCounter exchange_counter(fgc_exchange* x, uint32_t first, uint32_t per);
+PieceWait exchange_piece_wait(fgc_exchange* x, uint32_t first, uint32_t per, uint32_t target);
+uint32_t exchange_max_pieces();
+fgc_status exchange_join(fgc_exchange* x, cudaStream_t s);
+fgc_status exchange_events(fgc_exchange* x, uint32_t P, std::vector<cudaEvent_t>** ev);
+void exchange_counters(fgc_exchange* x, uint32_t** counter, uint64_t** step, int* nranks, int* rank,
+                       uint64_t* msg_bytes);
+bool exchange_ready(const fgc_exchange* x);
+void exchange_trace(cudaStream_t s, const char* tag);
 
 }  // namespace fgc

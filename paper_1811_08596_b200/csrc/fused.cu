@@ -159,6 +159,7 @@ struct CompressArgs {
   float2* dbg_spec;      // debug hook: write the spectrum and stop
   uint32_t count;        // chunks in this launch
   uint32_t ahead;        // L2 prefetch distance in chunks (one wave)
+  PieceCounter pc;       // exchange: per-piece completed-segment counters (optional)
 };
 
 struct __align__(16) CompressShared {
@@ -669,8 +670,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     seg[1] = 0; seg[2] = 0; seg[3] = 0;
     if (used > ci.code_cap) atomicOr(a.flags, FGC_FLAG_CAPACITY);
   }
-  if (fold) cluster.sync();                       // G: CTA 0 finished reading CTA 1's staging
-  else asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (a.pc.cnt) {
+    // the segment is complete once both CTAs' writes are visible device-wide
+    __threadfence();
+    if (!fold) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // the early arrive's phase
+    cluster.sync();                               // (G) every thread of both CTAs has fenced
+    if (r == 0 && tid == 0) atomicAdd(&a.pc.cnt[(chunk - a.pc.first) / a.pc.per], 1u);
+  } else if (fold) {
+    cluster.sync();                               // G: CTA 0 finished reading CTA 1's staging
+  } else {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   FGC_TS(6);
 }
 
@@ -691,6 +701,7 @@ struct DecodeArgs {
   const float2* spectrum;     // dense-spectrum mode (debug hook), else null
   uint32_t count;             // chunks in this launch
   uint32_t ahead;             // L2 prefetch distance in chunks (one wave)
+  PieceWait pw;               // exchange: wait for the peers' pieces (optional)
 };
 
 constexpr int kDecBatch = 4;                           // messages per block scan in the decode
@@ -773,6 +784,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   const uint32_t blk = dec_block(r, tid);                  // my 32-bin block
   const bool binN = (r == 0 && tid == kThreads - 1);       // also owns bin N (local slot 16384)
   float2* mine = acc + pad(32u * tid);                     // pad(32 t + j) = pad(32 t) + j
+  if (a.pw.flags) {
+    // peer exchange: every peer's copy of this chunk's piece has landed
+    if (tid < (uint32_t)a.pw.nranks && (int)tid != a.pw.me) {
+      const uint32_t* f = a.pw.flags + tid * a.pw.stride + (chunk - a.pw.first) / a.pw.per;
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if ((int32_t)(v - a.pw.target) >= 0) break;
+        __nanosleep(128);
+      }
+    }
+    __syncthreads();
+  }
   if (!a.spectrum && tid < (uint32_t)a.W && blockIdx.x / 2 + a.ahead < a.count) {
     // message segments of the chunk the next wave decodes here (CTA r: half of each)
     const ChunkInfo cn = a.chunks[chunk + a.ahead];
@@ -1046,9 +1070,10 @@ void fused_tables_free(FusedTables* t) {
 static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first,
                                        uint32_t count, const void* grad, int dtype, int half_pass,
                                        const QuantParams& q, uint8_t* message, uint32_t* flags, uint32_t* fb,
-                                       float2* fb_spec, float2* dbg, cudaStream_t s) {
+                                       float2* fb_spec, float2* dbg, cudaStream_t s, PieceCounter pc) {
   if (!count) return FGC_OK;
-  CompressArgs a{d_chunks, first, grad, q, message, flags, t->thi, t->tlo, t->t1024, fb, fb_spec, dbg, count, t->wave};
+  CompressArgs a{d_chunks, first, grad, q, message, flags, t->thi, t->tlo, t->t1024, fb, fb_spec, dbg, count, t->wave,
+                 pc};
   const size_t smem = sizeof(CompressShared);
   const dim3 grid(2 * count), block(kThreads);
   const bool f64 = dtype == FGC_DTYPE_F64, h = half_pass != 0;
@@ -1068,13 +1093,13 @@ static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_
 fgc_status launch_fused_compress(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                  const void* grad, int dtype, int half_pass, const QuantParams& q,
                                  uint8_t* message, uint32_t* flags, uint32_t* fb, float2* fb_spec,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, PieceCounter pc) {
   if (q.n_bits > 16) {
     set_error("fused kernels take N <= 16");
     return FGC_ERR_UNSUPPORTED;
   }
   return launch_compress_impl(t, d_chunks, first, count, grad, dtype, half_pass, q, message, flags, fb, fb_spec,
-                              nullptr, s);
+                              nullptr, s, pc);
 }
 
 fgc_status launch_fused_spectrum(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
@@ -1083,14 +1108,15 @@ fgc_status launch_fused_spectrum(const FusedTables* t, const ChunkInfo* d_chunks
   QuantParams q{};
   q.n_bits = 8;
   return launch_compress_impl(t, d_chunks, first, count, grad, dtype, half_pass, q, nullptr, flags, nullptr,
-                              nullptr, spectrum, s);
+                              nullptr, spectrum, s, PieceCounter());
 }
 
 fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
-                               const QuantParams& q, float* out, cudaStream_t s) {
+                               const QuantParams& q, float* out, cudaStream_t s, PieceWait pw) {
   if (!count) return FGC_OK;
-  DecodeArgs a{d_chunks, first, messages, W, stride, wts, q, out, t->thi, t->tlo, t->t1024, nullptr, count, t->wave};
+  DecodeArgs a{d_chunks, first, messages, W, stride, wts, q, out, t->thi, t->tlo, t->t1024, nullptr, count, t->wave,
+               pw};
   k_fused_decode<<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
   FGC_LAUNCHED(1);
   return FGC_OK;

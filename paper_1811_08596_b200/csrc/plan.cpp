@@ -635,6 +635,92 @@ extern "C" fgc_status fgc_allgather_average(fgc_plan* p, void* comm, int nranks,
   return FGC_OK;
 }
 
+// Wave-aligned pieces of the fused chunk range: [f[i], f[i+1]), the remainder
+// (< 2 pieces) in the last one; the generic (tail) chunks ride with the last.
+static std::vector<uint32_t> wave_pieces(const fgc_plan* p, uint32_t waves) {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t per = std::max(1u, waves * (uint32_t)(sms / 2));
+  const uint32_t P = waves ? std::max(1u, p->fused_count / per) : 1u;
+  std::vector<uint32_t> f(P + 1);
+  for (uint32_t i = 0; i < P; ++i) f[i] = p->fused_first + i * per;
+  f[P] = p->fused_first + p->fused_count;
+  return f;
+}
+
+extern "C" fgc_status fgc_exchange_average(fgc_plan* p, fgc_exchange* x, const void* grad, int dtype,
+                                           const double* weights, float* out, uint32_t* flags, void* stream) {
+  if (!p || !x || !grad || !out || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
+  if (!exchange_ready(x)) { set_error("exchange not opened"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_mode(p));
+  uint32_t* counter;
+  uint64_t* step;
+  int W, me;
+  uint64_t mb;
+  exchange_counters(x, &counter, &step, &W, &me, &mb);
+  if (mb != p->msg_bytes) { set_error("exchange sized for another plan"); return FGC_ERR_INVALID; }
+  Weights w;
+  FGC_TRY(fill_weights(weights, W, w));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<cudaEvent_t>* ev;
+  FGC_TRY(exchange_events(x, 1, &ev));
+  cudaEvent_t ev_start = (*ev)[0], ev_tail = (*ev)[1], ev_side = (*ev)[2];
+  const int k = (int)(*step & 1);
+  const uint32_t tval = (uint32_t)(*step + 1);          // this step's flag value
+  const uint32_t Pmax = exchange_max_pieces();
+  uint8_t *message, *gathered;
+  FGC_TRY(fgc_exchange_message(x, k, &message, &gathered));
+  exchange_trace(s, "start");
+  // generic (tail) chunks on the side stream from the start of the step:
+  // compress -> push (copy stream) -> wait for the peers' -> decode
+  const bool generic = p->classes.size() > (p->fused_count ? 1u : 0u);
+  const uint64_t fused_end = p->fused_count ? p->seg_off[p->fused_first + p->fused_count] : 0;
+  if (generic) {
+    FGC_CUDA(cudaEventRecord(ev_start, s));
+    FGC_CUDA(cudaStreamWaitEvent(p->side, ev_start, 0));
+    FGC_TRY(compress_range(p, grad, dtype, message, flags, p->side, 0, 0, true));
+    FGC_CUDA(cudaEventRecord(ev_tail, p->side));
+    exchange_trace(p->side, "tail-compressed");
+    FGC_TRY(exchange_publish_event(x, k, fused_end, p->msg_bytes - fused_end, ev_tail, tval));
+    FGC_TRY(exchange_wait(x, p->side, (int)Pmax, tval));
+    exchange_trace(p->side, "tail-arrived");
+    FGC_TRY(decode_range(p, gathered, W, p->msg_bytes, w, out, p->side, 0, 0, true));
+    exchange_trace(p->side, "tail-decoded");
+    FGC_CUDA(cudaEventRecord(ev_side, p->side));
+  }
+  if (p->fused_count) {
+    // one compress launch; the kernel counts finished chunks per piece and the
+    // copy streams push each piece the moment its count is complete
+    uint32_t P = 8;
+    if (const char* e = getenv("FGC_EXCHANGE_PIECES")) P = (uint32_t)std::max(1, atoi(e));
+    P = std::min(std::min(P, Pmax), p->fused_count);
+    const uint32_t per = (p->fused_count + P - 1) / P;
+    P = (p->fused_count + per - 1) / per;
+    const PieceCounter pc = exchange_counter(x, p->fused_first, per);
+    FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, p->fused_first, p->fused_count, grad, dtype,
+                                  p->desc.half_pass, p->q, message, flags, p->d_fb, p->d_spec, s, pc));
+    FGC_TRY(launch_select_pack(p->d_chunks, p->fused_first, p->fused_count, p->d_spec, 0, p->q, message, nullptr,
+                               flags, s, p->d_fb, pc));
+    exchange_trace(s, "compressed");
+    for (uint32_t i = 0; i < P; ++i) {
+      const uint32_t c0 = p->fused_first + i * per, c1 = std::min(p->fused_first + p->fused_count, c0 + per);
+      const uint64_t lo = p->seg_off[c0], hi = p->seg_off[c1];
+      FGC_TRY(exchange_publish_piece(x, k, i, lo, hi - lo, (uint32_t)((*step + 1) * (c1 - c0)), tval));
+    }
+    // one decode launch; each chunk's CTAs wait for their piece from every peer
+    FGC_TRY(launch_fused_decode(p->fused, p->d_chunks, p->fused_first, p->fused_count, gathered, W, p->msg_bytes,
+                                w, p->q, out, s, exchange_piece_wait(x, p->fused_first, per, tval)));
+    exchange_trace(s, "decoded");
+  }
+  if (generic) FGC_CUDA(cudaStreamWaitEvent(s, ev_side, 0));
+  FGC_TRY(exchange_join(x, s));
+  exchange_trace(s, "end");
+  *step += 1;
+  (void)counter;
+  return FGC_OK;
+}
+
 extern "C" const char* fgc_last_error(void) { return g_last_error.c_str(); }
 extern "C" int fgc_version(void) { return 0x000100; }
 extern "C" uint64_t fgc_kernel_launches(void) { return g_launches.load(); }

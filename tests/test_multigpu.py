@@ -1,7 +1,8 @@
-"""Compressed average across real GPUs: NCCL allgather of the fixed-capacity
-device messages over NVLink, then every rank decodes the W messages in worker
-order (simulator.py:520-547 with a real exchange).  Needs >= 2 GPUs; the
-2-rank host logic is covered on CPU by test_comm_cpu.py."""
+"""Compressed average across real GPUs: the fixed-capacity device messages
+move over NVLink (peer-to-peer copies through CUDA IPC, or one NCCL
+allgather), then every rank decodes the W messages in worker order
+(simulator.py:520-547 with a real exchange).  Needs >= 2 GPUs; the 2-rank
+host logic is covered on CPU by test_comm_cpu.py."""
 
 import os
 import socket
@@ -22,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, out_q):
+def _worker(rank, world, port, n, transport, out_q):
     import torch.distributed as dist
 
     import oracle as O
@@ -40,19 +41,22 @@ def _worker(rank, world, port, n, out_q):
         cfg = F.CodecConfig(F.SparsificationSpec(0.9), q)
         comm = NcclComm()
         w = F.shard_weights(5 * world + 1, world)
-        avg = GradientAverager(n, cfg, w, comm)
-        out = avg.step(torch.from_numpy(rows[rank]).cuda())
+        avg = GradientAverager(n, cfg, w, comm, transport=transport)
+        g = torch.from_numpy(rows[rank]).cuda()
+        outs = []
+        for _ in range(3):                      # the peer exchange alternates two gather buffers
+            outs.append(avg.step(g).clone())
         avg.check()
-        got = out.double().cpu().numpy()
+        got = outs[0].double().cpu().numpy()
+        for o in outs[1:]:
+            assert torch.equal(o, outs[0]), "steps disagree"
+        avg.close()
         # oracle: decode every rank's message (the wire bytes of this rank's
         # own compress are bit-identical on all ranks, so serialize locally)
         msgs = [F.compress(rows[k], cfg) for k in range(world)]
         ref = sum(w[k] * O.decompress(O.from_wire(F.serialize(msgs[k]))) for k in range(world))
         rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
         # every rank must hold bit-identical results
-        t = torch.from_numpy(got).cuda()
-        gathered = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(gathered, t.cpu()) if False else None
         digest = float(np.frombuffer(got.tobytes(), dtype=np.uint64).astype(np.float64).sum())
         out_q.put((rank, rel, digest))
         comm.close()
@@ -60,14 +64,15 @@ def _worker(rank, world, port, n, out_q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
 @pytest.mark.parametrize("n", [3 * 65536 + 40960, 1_000_000])
-def test_nccl_allgather_average_two_ranks(n):
+def test_compressed_average_two_ranks(n, transport):
     import torch.multiprocessing as mp
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, transport, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
