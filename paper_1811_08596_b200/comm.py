@@ -93,17 +93,38 @@ class PeerExchange:
         import torch.distributed as dist
         D.require_cuda()
         self.rank, self.world = rank, world
-        h = C.c_void_p()
-        _lib.check(_lib.lib.fgc_exchange_create(world, rank, message_bytes, C.byref(h)))
-        self.handle = h
-        mine = np.zeros(128, dtype=np.uint8)
-        _lib.check(_lib.lib.fgc_exchange_handles(h, mine.ctypes.data))
-        allh = [None] * world
-        dist.all_gather_object(allh, mine.tobytes(), group=group)
-        buf = np.frombuffer(b"".join(allh), dtype=np.uint8).copy()
-        _lib.check(_lib.lib.fgc_exchange_open(h, buf.ctypes.data))
-        dist.barrier(group)
         self._group = group
+        self.handle = None
+        # every step of the setup is agreed on by all ranks, so a failure on any
+        # rank (no IPC, no stream memory operations) fails all of them alike
+        h = C.c_void_p()
+        mine, err = None, ""
+        try:
+            _lib.check(_lib.lib.fgc_exchange_create(world, rank, message_bytes, C.byref(h)))
+            self.handle = h
+            mine = np.zeros(128, dtype=np.uint8)
+            _lib.check(_lib.lib.fgc_exchange_handles(h, mine.ctypes.data))
+            mine = mine.tobytes()
+        except Exception as e:                  # noqa: BLE001 -- reported below, on every rank
+            err = f"rank {rank}: {e}"
+        allh = [None] * world
+        dist.all_gather_object(allh, (mine, err), group=group)
+        errs = [e for _, e in allh if e]
+        if not errs:
+            try:
+                buf = np.frombuffer(b"".join(m for m, _ in allh), dtype=np.uint8).copy()
+                _lib.check(_lib.lib.fgc_exchange_open(h, buf.ctypes.data))
+            except Exception as e:              # noqa: BLE001
+                err = f"rank {rank}: {e}"
+            oks = [None] * world
+            dist.all_gather_object(oks, err, group=group)
+            errs = [e for e in oks if e]
+        if errs:
+            if self.handle:
+                _lib.lib.fgc_exchange_destroy(self.handle)
+                self.handle = None
+            raise RuntimeError("peer exchange unavailable: " + "; ".join(errs))
+        dist.barrier(group)
 
     def close(self) -> None:
         if getattr(self, "handle", None):
@@ -150,7 +171,12 @@ class GradientAverager:
             raise ValueError(f"unknown transport {self.transport!r}")
         self.exchange = None
         if self.world > 1 and self.transport == "peer":
-            self.exchange = PeerExchange(self.plan.message_bytes, comm.rank, comm.world, comm.group)
+            try:
+                self.exchange = PeerExchange(self.plan.message_bytes, comm.rank, comm.world, comm.group)
+            except RuntimeError as e:           # agreed on by every rank: all fall back together
+                import warnings
+                warnings.warn(f"{e}; using the NCCL allgather")
+                self.transport = "nccl"
 
     def close(self) -> None:
         if self.exchange is not None:
