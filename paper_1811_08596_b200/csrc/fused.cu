@@ -621,22 +621,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   for (uint32_t k = tid; k < nwords; k += kThreads) stg[k] = 0u;
   __syncthreads();
   {
-    uint64_t lbit = o + (uint64_t)base * N;               // local bit of my first code
-    auto emit_word_bits = [&](uint32_t word, uint32_t jbase) {
-      while (word) {
-        const uint32_t pos = __ffs(word) - 1;
-        word &= word - 1;
-        const uint32_t pc = arr_own[pad(32u * tid + jbase + (pos >> 1))];
+    uint32_t lbit = o + base * (uint32_t)N;               // local bit of my first code
+    const uint32_t* row = arr_own + pad(32u * tid);       // my 32 bins (pad(32t + j) = pad(32t) + j)
+    uint8_t* stg8 = reinterpret_cast<uint8_t*>(stg);
+    // slot s of my bins: bin s / 2, re (s even) / im (s odd); one loop over all 64 slots
+    auto emit_slots = [&](uint64_t m64, const uint32_t* src) {
+      while (m64) {
+        const uint32_t pos = __ffsll((long long)m64) - 1;
+        m64 &= m64 - 1;
+        const uint32_t pc = src[pos >> 1];
         const uint32_t code = (pos & 1) ? (pc >> 16) : (pc & 0xFFFFu);
-        const uint32_t wi = (uint32_t)(lbit >> 5), sb = (uint32_t)(lbit & 31u);
-        atomicOr(&stg[wi], code << sb);
-        if (sb + N > 32u) atomicOr(&stg[wi + 1], code >> (32u - sb));
+        if (N == 8) {
+          stg8[lbit >> 3] = (uint8_t)code;                // byte-aligned codes: plain stores
+        } else {
+          const uint32_t wi = lbit >> 5, sb = lbit & 31u;
+          atomicOr(&stg[wi], code << sb);
+          if (sb + N > 32u) atomicOr(&stg[wi + 1], code >> (32u - sb));
+        }
         lbit += N;
       }
     };
-    emit_word_bits(w0, 0);
-    emit_word_bits(w1, 16);
-    emit_word_bits(w2, 32);
+    emit_slots(((uint64_t)w1 << 32) | w0, row);
+    if (w2) emit_slots(w2, arr_own + pad(32u * tid + 32u));
   }
   __syncthreads();
   if (fold) {
