@@ -283,13 +283,7 @@ def _pack_host(m: CompressedMessage) -> tuple:
 
 # ------------------------------------------------------------------ pipeline
 
-def _check_count_mode(config: CodecConfig) -> None:
-    if config.sparsification.mode != "count":
-        raise NotImplementedError("energy-mode selection is not implemented on the GPU")
-
-
 def _compress_device(t: torch.Tensor, code: int, config: CodecConfig) -> tuple:
-    _check_count_mode(config)
     spec = config.sparsification
     plan = get_plan(t.numel(), config.chunk_size, spec.theta, spec.mode, config.half_precision_pass,
                     config.quantizer)

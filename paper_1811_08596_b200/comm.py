@@ -146,8 +146,6 @@ class GradientAverager:
 
     def __init__(self, n: int, config: CodecConfig, weights, comm: NcclComm | None = None,
                  transport: str | None = None):
-        if config.sparsification.mode != "count":
-            raise NotImplementedError("energy-mode selection is not implemented on the GPU")
         dev = D.require_cuda()
         spec = config.sparsification
         self.n = int(n)

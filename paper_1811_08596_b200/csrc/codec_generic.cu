@@ -107,13 +107,14 @@ __device__ void bitonic(SelectShared& sh, uint32_t M, bool by_index) {
   }
 }
 
-enum SelMode : int { kKeepAll = 0, kDropAll = 1, kList = 2, kExact = 3 };
+enum SelMode : int { kKeepAll = 0, kDropAll = 1, kList = 2, kExact = 3, kMask = 4 };
 
 template <typename CT>
 __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* chunks, uint32_t first, Coeffs<CT> coeffs,
                                                              int exact_only, QuantParams q, uint8_t* message,
                                                              uint8_t* kept_mask, uint32_t* flags,
-                                                             const uint32_t* only_if, PieceCounter pc) {
+                                                             const uint32_t* only_if, PieceCounter pc,
+                                                             const uint8_t* drop_mask) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SelectShared& sh = *reinterpret_cast<SelectShared*>(smem_raw);
   if (only_if && only_if[first + blockIdx.x] == 0u) return;
@@ -125,7 +126,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
   cf.p += ci.bin_off;
 
   int mode = kList;
-  if (kdrop == 0) mode = kKeepAll;
+  if (drop_mask) mode = kMask;                  // energy mode: the drop set is given
+  else if (kdrop == 0) mode = kKeepAll;
   else if (kdrop >= B) mode = kDropAll;
 
   float band_lo = 0.f, band_hi = INFINITY;   // proxy band of undecided bins
@@ -267,6 +269,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
     unsigned long long key = 0;
     if (mode == kDropAll) {
       dropped = true;
+    } else if (mode == kMask) {
+      dropped = valid && drop_mask[ci.bin_off + i];
     } else if (mode == kList || mode == kExact) {
       const float p = proxy_key(re, im);
       const bool inband = all_band || (p >= band_lo && p < band_hi);
@@ -433,7 +437,8 @@ __global__ void __launch_bounds__(kDecThreads) k_decode_accumulate(const ChunkIn
 
 fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_t count, const void* spectrum,
                               int coeff_f64, const QuantParams& q, uint8_t* message, uint8_t* kept_mask,
-                              uint32_t* flags, cudaStream_t s, const uint32_t* only_if, PieceCounter pc) {
+                              uint32_t* flags, cudaStream_t s, const uint32_t* only_if, PieceCounter pc,
+                              const uint8_t* drop_mask) {
   if (!count) return FGC_OK;
   static bool attr = false;
   const size_t smem = sizeof(SelectShared);
@@ -445,11 +450,11 @@ fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_
   if (coeff_f64) {
     Coeffs<double2> c{static_cast<const double2*>(spectrum)};
     k_select_pack<double2><<<count, kSelThreads, smem, s>>>(d_chunks, first, c, 1, q, message, kept_mask, flags,
-                                                            only_if, pc);
+                                                            only_if, pc, drop_mask);
   } else {
     Coeffs<float2> c{static_cast<const float2*>(spectrum)};
     k_select_pack<float2><<<count, kSelThreads, smem, s>>>(d_chunks, first, c, 0, q, message, kept_mask, flags,
-                                                           only_if, pc);
+                                                           only_if, pc, drop_mask);
   }
   FGC_LAUNCHED(1);
   return FGC_OK;

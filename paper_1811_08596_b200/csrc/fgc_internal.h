@@ -153,10 +153,29 @@ struct PieceWait {
   int nranks = 0, me = 0;
 };
 
+// drop_mask (may be null): 1 byte per bin of the chunk-major spectrum; when
+// given it replaces the count-mode selection (energy mode).
 fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_t count, const void* spectrum,
                               int coeff_f64, const QuantParams& q, uint8_t* message, uint8_t* kept_mask,
                               uint32_t* flags, cudaStream_t s, const uint32_t* only_if = nullptr,
-                              PieceCounter pc = PieceCounter());
+                              PieceCounter pc = PieceCounter(), const uint8_t* drop_mask = nullptr);
+
+// Energy-mode drop sets (energy.cu).
+struct EnergyScratch {
+  double *keys = nullptr, *keys2 = nullptr, *energy = nullptr, *sorted_e = nullptr, *total = nullptr;
+  uint32_t *idx = nullptr, *idx2 = nullptr, *kcut = nullptr;
+  uint8_t* drop = nullptr;
+  int* offs = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  uint64_t cap_bins = 0;
+  uint32_t cap_chunks = 0;
+  fgc_status ensure(uint64_t bins, uint32_t chunks);
+  void free_all();
+};
+fgc_status energy_drop_mask(EnergyScratch& e, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
+                            uint64_t bin0, uint64_t nbins, uint32_t max_bins, const float2* spectrum, double theta,
+                            cudaStream_t s, const uint8_t** drop_out);
 
 // Decode + weighted accumulate of W messages into a chunk-major spectrum.
 struct Weights {

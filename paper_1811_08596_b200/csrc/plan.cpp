@@ -50,6 +50,7 @@ struct fgc_plan {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   FusedTables* fused = nullptr;
   uint32_t fused_first = 0, fused_count = 0;     // chunk range taken by fused kernels
+  EnergyScratch energy;              // energy-mode selection scratch (allocated on first use)
   // pipelined allgather-average: exchange stream + per-piece events (created on first use)
   cudaStream_t xstream = nullptr;
   std::vector<cudaEvent_t> ev_comp, ev_gath;
@@ -238,6 +239,7 @@ extern "C" fgc_status fgc_plan_create(const fgc_codec_desc* desc, fgc_plan** out
 extern "C" void fgc_plan_destroy(fgc_plan* p) {
   if (!p) return;
   for (RealClass& rc : p->classes) rc.free_all();
+  p->energy.free_all();
   if (p->fused) fused_tables_free(p->fused);
   cudaFree(p->d_chunks);
   cudaFree(p->d_spec);
@@ -295,11 +297,31 @@ static fgc_status forward_generic(fgc_plan* p, const void* grad, int dtype, floa
 }
 
 static fgc_status check_mode(const fgc_plan* p) {
-  if (p->desc.mode != FGC_MODE_COUNT) {
-    set_error("energy-mode selection is not implemented on the GPU yet");
-    return FGC_ERR_UNSUPPORTED;
+  if (p->desc.mode != FGC_MODE_COUNT && p->desc.mode != FGC_MODE_ENERGY) {
+    set_error("unknown sparsification mode");
+    return FGC_ERR_INVALID;
   }
   return FGC_OK;
+}
+
+// Energy mode (spectral.py:134-139): every chunk through the generic FFT
+// (energy plans take no fused class), the exact energy drop set, then the
+// common quantize + pack with the drop mask.  spectrum_in (chunk-major
+// float2) replaces the forward transform when given (stage injection).
+static fgc_status energy_compress(fgc_plan* p, const void* grad, int dtype, const float2* spectrum_in,
+                                  uint8_t* message, uint8_t* kept_mask, uint32_t* flags, cudaStream_t s) {
+  const float2* spec = spectrum_in;
+  if (!spec) {
+    FGC_TRY(forward_generic(p, grad, dtype, p->d_spec, flags, s, false));
+    spec = p->d_spec;
+  }
+  uint32_t max_bins = 1;
+  for (const ChunkInfo& ci : p->chunks) max_bins = std::max(max_bins, ci.bins);
+  const uint8_t* drop = nullptr;
+  FGC_TRY(energy_drop_mask(p->energy, p->d_chunks, 0, p->n_chunks, 0, p->spec_bins, max_bins, spec, p->desc.theta,
+                           s, &drop));
+  return launch_select_pack(p->d_chunks, 0, p->n_chunks, spec, 0, p->q, message, kept_mask, flags, s, nullptr,
+                            PieceCounter(), drop);
 }
 
 // Compress the fused chunks [f0, f0 + fc) and, when `generic`, every generic
@@ -336,6 +358,8 @@ extern "C" fgc_status fgc_compress(fgc_plan* p, const void* grad, int dtype, uin
                                    void* stream) {
   if (!p || !grad || !message || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
   FGC_TRY(check_mode(p));
+  if (p->desc.mode == FGC_MODE_ENERGY)
+    return energy_compress(p, grad, dtype, nullptr, message, nullptr, flags, static_cast<cudaStream_t>(stream));
   return compress_range(p, grad, dtype, message, flags, static_cast<cudaStream_t>(stream), p->fused_first,
                         p->fused_count, true);
 }
@@ -344,6 +368,9 @@ extern "C" fgc_status fgc_encode_spectrum(fgc_plan* p, const void* spectrum, uin
                                           uint32_t* flags, void* stream) {
   if (!p || !spectrum || !message || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
   FGC_TRY(check_mode(p));
+  if (p->desc.mode == FGC_MODE_ENERGY)
+    return energy_compress(p, nullptr, 0, static_cast<const float2*>(spectrum), message, kept_mask, flags,
+                           static_cast<cudaStream_t>(stream));
   return launch_select_pack(p->d_chunks, 0, p->n_chunks, spectrum, 0, p->q, message, kept_mask, flags,
                             static_cast<cudaStream_t>(stream));
 }
@@ -584,6 +611,14 @@ extern "C" fgc_status fgc_allgather_average(fgc_plan* p, void* comm, int nranks,
   Weights w;
   FGC_TRY(fill_weights(weights, nranks, w));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t wpp = 0;
+  if (const char* e = getenv("FGC_PIPELINE_WAVES")) wpp = (uint32_t)std::max(0, atoi(e));
+  if (wpp == 0 || p->desc.mode != FGC_MODE_COUNT || !p->fused_count) {
+    // one piece: compress, one allgather, decode
+    FGC_TRY(fgc_compress(p, grad, dtype, message, flags, stream));
+    FGC_TRY(fgc_allgather(comm, message, gathered, p->msg_bytes, stream));
+    return decode_range(p, gathered, nranks, p->msg_bytes, w, out, s, p->fused_first, p->fused_count, true);
+  }
   // Pipeline in P pieces of consecutive chunks (their segments are contiguous):
   // piece i is allgathered on the exchange stream while piece i+1 compresses,
   // and decoded once its exchange is done.  The gather buffer holds piece i of
@@ -596,8 +631,6 @@ extern "C" fgc_status fgc_allgather_average(fgc_plan* p, void* comm, int nranks,
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  uint32_t wpp = 0;
-  if (const char* e = getenv("FGC_PIPELINE_WAVES")) wpp = (uint32_t)std::max(0, atoi(e));
   const uint32_t per = std::max(1u, wpp * (uint32_t)(sms / 2));
   uint32_t P = wpp ? std::max(1u, p->fused_count / per) : 1u;
   std::vector<uint32_t> f(P + 1);
@@ -672,6 +705,17 @@ extern "C" fgc_status fgc_exchange_average(fgc_plan* p, fgc_exchange* x, const v
   uint8_t *message, *gathered;
   FGC_TRY(fgc_exchange_message(x, k, &message, &gathered));
   exchange_trace(s, "start");
+  if (p->desc.mode == FGC_MODE_ENERGY) {
+    // energy mode: no fused chunks; the whole message is one piece
+    FGC_TRY(energy_compress(p, grad, dtype, nullptr, message, nullptr, flags, s));
+    FGC_CUDA(cudaEventRecord(ev_tail, s));
+    FGC_TRY(exchange_publish_event(x, k, 0, p->msg_bytes, ev_tail, tval));
+    FGC_TRY(exchange_wait(x, s, (int)Pmax, tval));
+    FGC_TRY(decode_range(p, gathered, W, p->msg_bytes, w, out, s, 0, 0, true));
+    FGC_TRY(exchange_join(x, s));
+    *step += 1;
+    return FGC_OK;
+  }
   // generic (tail) chunks on the side stream from the start of the step:
   // compress -> push (copy stream) -> wait for the peers' -> decode
   const bool generic = p->classes.size() > (p->fused_count ? 1u : 0u);

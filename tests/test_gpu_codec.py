@@ -47,9 +47,9 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / (nb if nb else 1.0)
 
 
-def segments_valid_bytes(dev: bytes, n, chunk, theta, width):
+def segments_valid_bytes(dev: bytes, n, chunk, theta, width, mode="count"):
     """Per chunk: nnz, wire bitmap bytes, wire code bytes from a device message."""
-    layout, _ = O.device_layout(n, chunk, theta, width)
+    layout, _ = O.device_layout(n, chunk, theta, width, mode)
     out = []
     for (off, bmo, co, cap), L in zip(layout, O.chunk_lengths(n, chunk)):
         nnz = int.from_bytes(dev[off:off + 4], "little")
@@ -490,3 +490,54 @@ def test_resnet50_size_properties():
         ref = O.decompress(O.Message(L, 65536, 0.9, "count", False, lat_of(q), [ch]))
         assert rel_l2(out1[off:off + L].cpu().numpy(), ref) <= 1e-5
         assert rel_l2(np.fft.rfft(host[off:off + L]), spec[b0:b0 + L // 2 + 1]) <= 1e-6
+
+
+# ---------------------------------------------------------------- energy mode
+
+@pytest.mark.parametrize("theta", [0.0, 0.3, 0.7, 0.95, 1.0])
+@pytest.mark.parametrize("n,chunk,nm", [(3 * 65536 + 40960, 65536, (8, 3)), (5000, 1024, (6, 2)), (71, 16, None)])
+def test_energy_mode_injection_bit_exact(theta, n, chunk, nm):
+    """spectral.py:134-139 given identical coefficients: kept mask, bitmap and
+    codes equal the oracle's (numpy pairwise sum, stable order, sequential
+    cumulative energy)."""
+    rng = np.random.default_rng(int(theta * 100) + n)
+    lens = O.chunk_lengths(n, chunk)
+    spec = np.concatenate([(rng.standard_normal(L // 2 + 1) * rng.random(L // 2 + 1) ** 3
+                            + 1j * rng.standard_normal(L // 2 + 1)) for L in lens]).astype(np.complex64)
+    q = None if nm is None else F.tune_eps(-5.0, 5.0, *nm)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta, "energy"), q, chunk_size=chunk)
+    msg, mask = debug.encode_spectrum(spec, n, cfg)
+    got = segments_valid_bytes(debug.message_bytes(msg), n, chunk, theta, 32 if q is None else nm[0],
+                               mode="energy")
+    pos = 0
+    for L, (nnz, bm, cb) in zip(lens, got):
+        b = L // 2 + 1
+        kept, ch = O.encode_spectrum(spec[pos:pos + b], L, theta, "energy", lat_of(q))
+        np.testing.assert_array_equal(mask[pos:pos + b], kept)
+        nb = 32 if q is None else nm[0]
+        assert (nnz, bm, cb) == (ch.codes.size, O.flags_to_bytes(ch.bitmap), O.codes_to_bytes(ch.codes, nb))
+        pos += b
+
+
+def test_energy_mode_round_trip_and_wire():
+    rng = np.random.default_rng(5)
+    n, chunk = 2 * 65536 + 1000, 65536
+    g = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+    q = F.calibrate([g], 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.8, "energy"), q, chunk_size=chunk)
+    spec = debug.forward_spectrum(g, cfg)
+    msg = F.compress(g, cfg)
+    wire = F.serialize(msg)
+    back = F.deserialize(wire)
+    assert back.mode == "energy"
+    # the oracle's message from the GPU's own coefficients, byte for byte
+    ref = O.Message(n, chunk, float(np.float32(0.8)), "energy", False, lat_of(q), [])
+    pos = 0
+    for L in O.chunk_lengths(n, chunk):
+        b = L // 2 + 1
+        _, ch = O.encode_spectrum(spec[pos:pos + b], L, 0.8, "energy", lat_of(q))
+        ref.chunks.append(ch)
+        pos += b
+    assert wire == O.to_wire(ref)
+    got = F.decompress(msg)
+    assert rel_l2(got, O.decompress(ref)) <= 1e-5

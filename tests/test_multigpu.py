@@ -23,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, transport, out_q):
+def _worker(rank, world, port, n, transport, mode, out_q):
     import torch.distributed as dist
 
     import oracle as O
@@ -38,7 +38,7 @@ def _worker(rank, world, port, n, transport, out_q):
         rng = np.random.default_rng(77)
         rows = (rng.standard_normal((world, n)) * 1e-2).astype(np.float32)
         q = F.calibrate([rows[0]], 8, 3)
-        cfg = F.CodecConfig(F.SparsificationSpec(0.9), q)
+        cfg = F.CodecConfig(F.SparsificationSpec(0.9, mode), q)
         comm = NcclComm()
         w = F.shard_weights(5 * world + 1, world)
         avg = GradientAverager(n, cfg, w, comm, transport=transport)
@@ -64,15 +64,16 @@ def _worker(rank, world, port, n, transport, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("transport", ["peer", "nccl"])
+@pytest.mark.parametrize("transport,mode", [("peer", "count"), ("nccl", "count"), ("peer", "energy"),
+                                            ("nccl", "energy")])
 @pytest.mark.parametrize("n", [3 * 65536 + 40960, 1_000_000])
-def test_compressed_average_two_ranks(n, transport):
+def test_compressed_average_two_ranks(n, transport, mode):
     import torch.multiprocessing as mp
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, transport, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, transport, mode, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
