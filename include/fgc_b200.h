@@ -250,6 +250,11 @@ fgc_status fgc_irfft(const void* spectrum_c128, uint64_t L, double* signal, void
  * zeroed spectrum (may alias the input) and the kept mask (uint8/bin). */
 fgc_status fgc_truncate(const void* spectrum_c128, uint64_t bins, double theta, void* out_c128, uint8_t* kept_mask,
                         void* stream);
+/* truncate for either mode (spectral.py:124-156) of the half spectrum of an
+ * n-sample signal (bins = n/2 + 1; n's parity sets the Nyquist weight of
+ * the energy rule, bin_weights spectral.py:109-115). */
+fgc_status fgc_truncate_mode(const void* spectrum_c128, uint64_t bins, uint64_t n, double theta, int mode,
+                             void* out_c128, uint8_t* kept_mask, void* stream);
 
 /* calibrate's range reduction (codec.py:463-464): max over |Re|, |Im| of the
  * float64 rfft of one sample, max-accumulated into the device double *peak

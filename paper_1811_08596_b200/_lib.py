@@ -84,6 +84,7 @@ _SIGS = {
     "fgc_rfft": (I32, [P, I32, U64, P, P, P]),
     "fgc_irfft": (I32, [P, U64, P, P]),
     "fgc_truncate": (I32, [P, U64, F64, P, P, P]),
+    "fgc_truncate_mode": (I32, [P, U64, U64, F64, I32, P, P, P]),
     "fgc_spectrum_peak": (I32, [P, I32, U64, P, P, P]),
     "fgc_half_round_trip": (I32, [P, U64, P, P]),
     "fgc_nccl_unique_id": (I32, [P]),

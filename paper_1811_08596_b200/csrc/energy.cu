@@ -23,12 +23,13 @@ namespace fgc {
 namespace {
 
 // per bin: exact key, weighted energy, original index
-__global__ void k_energy_prep(const ChunkInfo* chunks, uint32_t first, const float2* spectrum, double* keys,
+template <class T2>
+__global__ void k_energy_prep(const ChunkInfo* chunks, uint32_t first, const T2* spectrum, double* keys,
                               uint32_t* idx, double* energy) {
   const ChunkInfo ci = chunks[first + blockIdx.y];
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= ci.bins) return;
-  const float2 x = spectrum[ci.bin_off + b];
+  const T2 x = spectrum[ci.bin_off + b];
   const double mag = cabs_key((double)x.x, (double)x.y);
   const bool single = (b == 0) || ((ci.len % 2u) == 0u && b == ci.bins - 1);   // DC / Nyquist weight 1
   keys[ci.bin_off + b] = mag;
@@ -182,12 +183,17 @@ void EnergyScratch::free_all() {
 // Drop mask (1 = dropped) for chunks [first, first + count) of a chunk-major
 // float2 spectrum whose bins start at bin_off(first) = bin0.
 fgc_status energy_drop_mask(EnergyScratch& e, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
-                            uint64_t bin0, uint64_t nbins, uint32_t max_bins, const float2* spectrum, double theta,
-                            cudaStream_t s, const uint8_t** drop_out) {
+                            uint64_t bin0, uint64_t nbins, uint32_t max_bins, const void* spectrum, int f64,
+                            double theta, cudaStream_t s, const uint8_t** drop_out) {
   if (!count) return FGC_OK;
   FGC_TRY(e.ensure(bin0 + nbins, count));
   const dim3 grid(cdiv32(max_bins, 256), count);
-  k_energy_prep<<<grid, 256, 0, s>>>(d_chunks, first, spectrum, e.keys, e.idx, e.energy);
+  if (f64)
+    k_energy_prep<double2><<<grid, 256, 0, s>>>(d_chunks, first, static_cast<const double2*>(spectrum), e.keys,
+                                                e.idx, e.energy);
+  else
+    k_energy_prep<float2><<<grid, 256, 0, s>>>(d_chunks, first, static_cast<const float2*>(spectrum), e.keys, e.idx,
+                                               e.energy);
   FGC_LAUNCHED(1);
   k_energy_total<<<cdiv32(count, 64), 64, 0, s>>>(d_chunks, first, count, e.energy, e.total);
   FGC_LAUNCHED(1);

@@ -174,8 +174,8 @@ struct EnergyScratch {
   void free_all();
 };
 fgc_status energy_drop_mask(EnergyScratch& e, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
-                            uint64_t bin0, uint64_t nbins, uint32_t max_bins, const float2* spectrum, double theta,
-                            cudaStream_t s, const uint8_t** drop_out);
+                            uint64_t bin0, uint64_t nbins, uint32_t max_bins, const void* spectrum, int f64,
+                            double theta, cudaStream_t s, const uint8_t** drop_out);
 
 // Decode + weighted accumulate of W messages into a chunk-major spectrum.
 struct Weights {

@@ -318,8 +318,8 @@ static fgc_status energy_compress(fgc_plan* p, const void* grad, int dtype, cons
   uint32_t max_bins = 1;
   for (const ChunkInfo& ci : p->chunks) max_bins = std::max(max_bins, ci.bins);
   const uint8_t* drop = nullptr;
-  FGC_TRY(energy_drop_mask(p->energy, p->d_chunks, 0, p->n_chunks, 0, p->spec_bins, max_bins, spec, p->desc.theta,
-                           s, &drop));
+  FGC_TRY(energy_drop_mask(p->energy, p->d_chunks, 0, p->n_chunks, 0, p->spec_bins, max_bins, spec, 0,
+                           p->desc.theta, s, &drop));
   return launch_select_pack(p->d_chunks, 0, p->n_chunks, spec, 0, p->q, message, kept_mask, flags, s, nullptr,
                             PieceCounter(), drop);
 }

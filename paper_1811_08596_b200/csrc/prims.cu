@@ -297,8 +297,8 @@ extern "C" fgc_status fgc_irfft(const void* spectrum, uint64_t L, double* signal
   return FGC_OK;
 }
 
-extern "C" fgc_status fgc_truncate(const void* spectrum, uint64_t bins, double theta, void* out, uint8_t* kept_mask,
-                                   void* stream) {
+static fgc_status truncate_impl(const void* spectrum, uint64_t bins, uint64_t n, double theta, int mode, void* out,
+                                uint8_t* kept_mask, void* stream) {
   if (!spectrum || !out || !kept_mask || bins < 1 || bins > 0x7FFFFFFFull) return FGC_ERR_INVALID;
   if (!(theta >= 0.0 && theta <= 1.0)) { set_error("theta must be in [0, 1]"); return FGC_ERR_INVALID; }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -306,7 +306,7 @@ extern "C" fgc_status fgc_truncate(const void* spectrum, uint64_t bins, double t
   ChunkInfo ci{};
   ci.bins = (uint32_t)bins;
   ci.slots = 2 * ci.bins;
-  ci.len = 2 * ((uint32_t)bins - 1);
+  ci.len = (uint32_t)n;
   ci.drop = (uint32_t)ceil(theta * (double)bins);
   if (ci.drop > bins) ci.drop = (uint32_t)bins;
   const uint64_t bm_words = (ci.slots + 31) / 32;
@@ -316,6 +316,7 @@ extern "C" fgc_status fgc_truncate(const void* spectrum, uint64_t bins, double t
   ChunkInfo* d_ci = nullptr;
   uint8_t* d_msg = nullptr;
   uint32_t* d_flags = nullptr;
+  EnergyScratch es;
   fgc_status st = FGC_OK;
   cudaError_t e;
   if ((e = cudaMalloc(&d_ci, sizeof(ChunkInfo))) != cudaSuccess) st = cuda_check(e, "cudaMalloc");
@@ -323,10 +324,14 @@ extern "C" fgc_status fgc_truncate(const void* spectrum, uint64_t bins, double t
   if (st == FGC_OK && (e = cudaMalloc(&d_flags, 4)) != cudaSuccess) st = cuda_check(e, "cudaMalloc");
   if (st == FGC_OK && (e = cudaMemcpyAsync(d_ci, &ci, sizeof(ci), cudaMemcpyHostToDevice, s)) != cudaSuccess)
     st = cuda_check(e, "cudaMemcpyAsync");
+  const uint8_t* drop = nullptr;
+  if (st == FGC_OK && mode == FGC_MODE_ENERGY)
+    st = energy_drop_mask(es, d_ci, 0, 1, 0, bins, (uint32_t)bins, spectrum, 1, theta, s, &drop);
   if (st == FGC_OK) {
     QuantParams q{};
     q.n_bits = 32;
-    st = launch_select_pack(d_ci, 0, 1, spectrum, 1, q, d_msg, kept_mask, d_flags, s);
+    st = launch_select_pack(d_ci, 0, 1, spectrum, 1, q, d_msg, kept_mask, d_flags, s, nullptr, PieceCounter(),
+                            drop);
   }
   if (st == FGC_OK) {
     k_zero_dropped<<<cdiv(bins, 256), 256, 0, s>>>(static_cast<const double2*>(spectrum), kept_mask, bins,
@@ -338,7 +343,20 @@ extern "C" fgc_status fgc_truncate(const void* spectrum, uint64_t bins, double t
   cudaFree(d_ci);
   cudaFree(d_msg);
   cudaFree(d_flags);
+  es.free_all();
   return st;
+}
+
+extern "C" fgc_status fgc_truncate(const void* spectrum, uint64_t bins, double theta, void* out, uint8_t* kept_mask,
+                                   void* stream) {
+  return truncate_impl(spectrum, bins, 2 * (bins - 1), theta, FGC_MODE_COUNT, out, kept_mask, stream);
+}
+
+extern "C" fgc_status fgc_truncate_mode(const void* spectrum, uint64_t bins, uint64_t n, double theta, int mode,
+                                        void* out, uint8_t* kept_mask, void* stream) {
+  if (mode != FGC_MODE_COUNT && mode != FGC_MODE_ENERGY) { set_error("unknown mode"); return FGC_ERR_INVALID; }
+  if (n / 2 + 1 != bins) { set_error("bins must be n // 2 + 1"); return FGC_ERR_INVALID; }
+  return truncate_impl(spectrum, bins, n, theta, mode, out, kept_mask, stream);
 }
 
 extern "C" fgc_status fgc_spectrum_peak(const void* signal, int dtype, uint64_t L, double* peak, uint32_t* flags,

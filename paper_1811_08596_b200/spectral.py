@@ -99,19 +99,20 @@ def spectrum_energy(spectrum: Spectrum) -> float:
 
 
 def truncate(spectrum: Spectrum, spec: SparsificationSpec) -> tuple[Spectrum, np.ndarray]:
-    """spectral.py:142-156, count mode on the GPU: zero the ceil(theta*bins)
-    smallest-magnitude bins (ties to the lower index)."""
+    """spectral.py:142-156 on the GPU.  count: zero the ceil(theta*bins)
+    smallest-magnitude bins (ties to the lower index); energy: zero the
+    smallest bins whose cumulative Parseval energy stays within theta**2 of
+    the total (spectral.py:134-139)."""
     if spec.domain != "frequency":
         raise ValueError(f"truncate expects a frequency-domain spec, got {spec.domain!r}")
-    if spec.mode != "count":
-        raise NotImplementedError("energy-mode truncation is not implemented on the GPU")
     dev = D.require_cuda()
     bins = spectrum.bins
     src = torch.from_numpy(np.ascontiguousarray(spectrum.coefficients).view(np.float64).copy()).to(dev)
     out = torch.empty_like(src)
     mask = torch.empty(bins, dtype=torch.uint8, device=dev)
-    _lib.check(_lib.lib.fgc_truncate(src.data_ptr(), bins, float(spec.theta), out.data_ptr(),
-                                     mask.data_ptr(), D.stream()))
+    mode = _lib.MODE_ENERGY if spec.mode == "energy" else _lib.MODE_COUNT
+    _lib.check(_lib.lib.fgc_truncate_mode(src.data_ptr(), bins, spectrum.n, float(spec.theta), mode, out.data_ptr(),
+                                          mask.data_ptr(), D.stream()))
     coeffs = out.cpu().numpy().view(np.complex128).reshape(-1)
     return Spectrum(coeffs, spectrum.n), mask.cpu().numpy().astype(bool)
 

@@ -541,3 +541,21 @@ def test_energy_mode_round_trip_and_wire():
     assert wire == O.to_wire(ref)
     got = F.decompress(msg)
     assert rel_l2(got, O.decompress(ref)) <= 1e-5
+
+
+@pytest.mark.parametrize("n", [8, 9, 1000, 1001, 65536, 100_003])
+@pytest.mark.parametrize("theta", [0.0, 0.5, 0.9, 1.0])
+def test_truncate_energy_mode_complex128(n, theta):
+    """spectral.truncate with mode "energy" on complex128 coefficients: the
+    GPU drop set equals the oracle's (Parseval weights by n's parity)."""
+    rng = np.random.default_rng(n)
+    b = n // 2 + 1
+    c = rng.standard_normal(b) + 1j * rng.standard_normal(b)
+    c[rng.integers(0, b, size=max(1, b // 10))] = 0.25 + 0.5j         # ties
+    out, mask = F.truncate(F.Spectrum(c, n), F.SparsificationSpec(theta, "energy"))
+    mag = np.abs(c)
+    dropped = O.drop_set(mag, O.parseval_weights(n) * mag ** 2, theta, "energy")
+    ref = np.ones(b, dtype=bool)
+    ref[dropped] = False
+    np.testing.assert_array_equal(mask, ref)
+    np.testing.assert_array_equal(out.coefficients, np.where(mask, c, 0))
