@@ -164,8 +164,8 @@ struct CompressArgs {
 
 struct __align__(16) CompressShared {
   float2 buf[kPadded + 64];          // FFT transposes / 4 sub-histograms / bin-ordered code half + staging
-  float2 thi[256], tlo[256];
-  float2 t1024[1024];
+  float2 thi[256], tlo[kTloPadded];   // tlo and t1024 in tpad layout
+  float2 t1024[kT1024Padded];
   uint32_t hist[2048];               // pass-1 histogram of this CTA (read by the peer)
   uint32_t hist2[2048];              // pass-2 histogram of this CTA (read by the peer)
   uint32_t scan[40];
@@ -297,10 +297,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   }
   if (tid < 256) {
     sh.thi[tid] = a.thi[tid];
-    sh.tlo[tid] = a.tlo[tid];
+    sh.tlo[tpad(tid)] = a.tlo[tid];
   }
-  sh.t1024[tid] = a.t1024[tid];
-  sh.t1024[tid + 512] = a.t1024[tid + 512];
+  sh.t1024[tpad(tid)] = a.t1024[tid];
+  sh.t1024[tpad(tid + 512)] = a.t1024[tid + 512];
   reinterpret_cast<uint4*>(sh.hist2)[tid] = make_uint4(0, 0, 0, 0);
   if (tid == 0) { sh.ccount = 0; sh.below = 0; sh.anynz = 0; sh.rcount[0] = 0; sh.rcount[1] = 0; }
   uint32_t* codes_g = DEBUG ? nullptr : reinterpret_cast<uint32_t*>(a.message + ci.seg_off + ci.code_off);
@@ -714,8 +714,8 @@ constexpr int kDecBatch = 4;                           // messages per block sca
 
 struct __align__(16) DecodeShared {
   float2 x[kPadded + 64];            // this CTA's bins of the weighted spectrum sum, then Y_r / FFT scratch
-  float2 thi[256], tlo[256];
-  float2 t1024[1024];
+  float2 thi[256], tlo[kTloPadded];   // tlo and t1024 in tpad layout
+  float2 t1024[kT1024Padded];
   uint32_t bm[kDecBatch][2 * kThreads * 2];   // natural-order bitmap words 0..2047 of a message batch
   uint32_t pref[kDecBatch][2 * kThreads];     // codes before each 32-bin block
   uint32_t bmN[kDecBatch];                    // word 2048 (bin N)
@@ -781,10 +781,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   const uint32_t tid = threadIdx.x;
   if (tid < 256) {
     sh.thi[tid] = a.thi[tid];
-    sh.tlo[tid] = a.tlo[tid];
+    sh.tlo[tpad(tid)] = a.tlo[tid];
   }
-  sh.t1024[tid] = a.t1024[tid];
-  sh.t1024[tid + 512] = a.t1024[tid + 512];
+  sh.t1024[tpad(tid)] = a.t1024[tid];
+  sh.t1024[tpad(tid + 512)] = a.t1024[tid + 512];
   float2* acc = sh.x;
   const uint32_t dbg = g_fused_dbg;
   const uint32_t blk = dec_block(r, tid);                  // my 32-bin block

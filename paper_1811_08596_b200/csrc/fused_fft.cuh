@@ -23,6 +23,13 @@ constexpr uint32_t kPadded = kM + kM / 32;
 
 __device__ __forceinline__ uint32_t pad(uint32_t e) { return e + (e >> 5); }
 
+// Twiddle tables in shared memory are stored with one spare entry per 8, so
+// the strided lookups of the FFT passes (index j*k over the lanes k) spread
+// over the banks: tpad(m) = m + m/8.
+__host__ __device__ constexpr uint32_t tpad(uint32_t m) { return m + (m >> 3); }
+constexpr uint32_t kTloPadded = 256 + 32;
+constexpr uint32_t kT1024Padded = 1024 + 128;
+
 // cos / sin (2 pi m / 32), m = 0..15
 __device__ constexpr float kC32[16] = {1.0f, 0.98078528040323043f, 0.92387953251128674f, 0.83146961230254524f,
                                         0.70710678118654752f, 0.55557023301960222f, 0.38268343236508977f,
@@ -111,7 +118,7 @@ __device__ __forceinline__ float2 w32mul(float2 d) {
 
 // W_65536^m from the two-level table (m taken mod 65536).
 __device__ __forceinline__ float2 tw(const float2* thi, const float2* tlo, uint32_t m) {
-  return cmul(thi[(m >> 8) & 255u], tlo[m & 255u]);
+  return cmul(thi[(m >> 8) & 255u], tlo[tpad(m & 255u)]);
 }
 __device__ __forceinline__ float2 twc(const float2* thi, const float2* tlo, uint32_t m, bool inv) {
   float2 w = tw(thi, tlo, m);
@@ -136,7 +143,7 @@ __device__ __forceinline__ void fft_pass12(float2 (&v)[32], float2* buf, const f
   const uint32_t k = i & 31u;
 #pragma unroll
   for (int j = 1; j < 32; ++j) {                   // W_1024^{jk}, jk < 1024
-    float2 w = t1024[j * k];
+    float2 w = t1024[tpad(j * k)];
     if (INV) w.y = -w.y;
     v[j] = cmul(v[j], w);
   }
