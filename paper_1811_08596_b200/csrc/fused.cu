@@ -536,7 +536,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   uint32_t* arr_own = reinterpret_cast<uint32_t*>(sh.buf);
   uint32_t* arr_peer = reinterpret_cast<uint32_t*>(shp.buf);
   uint32_t rc0 = 0, rc1 = 0;                      // my non-zero codes per half
-  auto emit_pair = [&](float2 x, uint32_t bin) {
+  // half d of bin (2k + r) + 2048 j is j >= 8 for both columns (and 1 for bin N):
+  // a compile-time choice, so own-half stores stay STS and the peer's go to DSMEM
+  auto emit_pair = [&](float2 x, uint32_t bin, auto D) {
+    constexpr uint32_t d = decltype(D)::value;
     const float p = proxy_key(x.x, x.y);
     bool keep = p >= lo_b;
     if (keep && p < hi_b) keep = !inband_dropped(&sh0, mcount, bin);
@@ -544,20 +547,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       const uint32_t cre = enc16(q, x.x), cim = enc16(q, x.y);
       const uint32_t pc = cre | (cim << 16);
       if (pc) {
-        const uint32_t d = bin >= kHalfBins ? 1u : 0u;
         const uint32_t c = (cre ? 1u : 0u) + (cim ? 1u : 0u);
         if (d) rc1 += c; else rc0 += c;
-        uint32_t* dst = (d == r) ? arr_own : arr_peer;
-        dst[pad(bin - d * kHalfBins)] = pc;
+        const uint32_t e = pad(bin - d * kHalfBins);
+        if (d == r) arr_own[e] = pc;
+        else arr_peer[e] = pc;
       }
     }
   };
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    emit_pair(va[j], BIN_A(j));
-    emit_pair(vb[j], BIN_B(j));
-  }
-  if (special) emit_pair(xn, kN);
+  static_for<0, 16>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    emit_pair(va[j], BIN_A(j), std::integral_constant<uint32_t, (j >= 8 ? 1u : 0u)>{});
+    emit_pair(vb[j], BIN_B(j), std::integral_constant<uint32_t, (j >= 8 ? 1u : 0u)>{});
+  });
+  if (special) emit_pair(xn, kN, std::integral_constant<uint32_t, 1u>{});
 #undef BIN_A
 #undef BIN_B
   {
