@@ -166,6 +166,7 @@ struct __align__(16) CompressShared {
   float2 buf[kPadded + 64];          // FFT transposes / 4 sub-histograms / bin-ordered code half + staging
   float2 thi[256], tlo[kTloPadded];   // tlo and t1024 in tpad layout
   float2 t1024[kT1024Padded];
+  uint32_t hbm[1024 + 4];            // bitmap of this CTA's half (natural slot order), set during emit
   uint32_t hist[2048];               // pass-1 histogram of this CTA (read by the peer)
   uint32_t hist2[2048];              // pass-2 histogram of this CTA (read by the peer)
   uint32_t scan[40];
@@ -302,6 +303,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   sh.t1024[tpad(tid)] = a.t1024[tid];
   sh.t1024[tpad(tid + 512)] = a.t1024[tid + 512];
   reinterpret_cast<uint4*>(sh.hist2)[tid] = make_uint4(0, 0, 0, 0);
+  sh.hbm[tid] = 0u;
+  sh.hbm[tid + 512] = 0u;
+  if (tid < 4) sh.hbm[1024 + tid] = 0u;
   if (tid == 0) { sh.ccount = 0; sh.below = 0; sh.anynz = 0; sh.rcount[0] = 0; sh.rcount[1] = 0; }
   uint32_t* codes_g = DEBUG ? nullptr : reinterpret_cast<uint32_t*>(a.message + ci.seg_off + ci.code_off);
   __syncthreads();
@@ -459,7 +463,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       }
       __syncthreads();
     }
-    zero_buf(sh, (kPadded + 64) / 2);             // code arrays: sub-histograms are merged
     FGC_TS(8);
     cluster.sync();                               // B: pass-2 histograms visible, buf zeroed
     if (mode == kModeList) {
@@ -509,8 +512,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     mode = sh0.mode;
     mcount = (mode == kModeList) ? sh0.ccount : 0u;
   } else {
-    zero_buf(sh, (kPadded + 64) / 2);
-    cluster.sync();                               // D': both code arrays zeroed
+    cluster.sync();                               // D': both bitmaps zeroed (peer atomics follow)
   }
 
   FGC_TS(4);
@@ -549,9 +551,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       if (pc) {
         const uint32_t c = (cre ? 1u : 0u) + (cim ? 1u : 0u);
         if (d) rc1 += c; else rc0 += c;
-        const uint32_t e = pad(bin - d * kHalfBins);
-        if (d == r) arr_own[e] = pc;
-        else arr_peer[e] = pc;
+        const uint32_t lb = bin - d * kHalfBins;
+        const uint32_t bits = ((cre ? 1u : 0u) | (cim ? 2u : 0u)) << (2u * (lb & 15u));
+        if (d == r) {
+          arr_own[pad(lb)] = pc;
+          atomicOr(&sh.hbm[lb >> 4], bits);
+        } else {
+          arr_peer[pad(lb)] = pc;
+          atomicOr(&shp.hbm[lb >> 4], bits);
+        }
       }
     }
   };
@@ -585,21 +593,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 
   // ---- 6. pack: thread t of CTA d owns bins d*16384 + [32t, 32t+32) (+ bin N)
   const uint32_t nb = (r == 1 && tid == kThreads - 1) ? 33u : 32u;
-  uint32_t w0 = 0, w1 = 0, w2 = 0;
-  {
-    const uint32_t* src = arr_own + pad(32u * tid);    // pad(32t + j) = pad(32t) + j
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const uint32_t pc = src[j];
-      const uint32_t bits = ((pc & 0xFFFFu) ? 1u : 0u) | ((pc >> 16) ? 2u : 0u);
-      if (j < 16) w0 |= bits << (2 * j);
-      else w1 |= bits << (2 * (j - 16));
-    }
-    if (nb == 33) {
-      const uint32_t pc = arr_own[pad(32u * tid + 32u)];
-      w2 = ((pc & 0xFFFFu) ? 1u : 0u) | ((pc >> 16) ? 2u : 0u);
-    }
-  }
+  // the bitmap was built during emit; only the set slots of the code arrays are valid
+  const uint32_t w0 = sh.hbm[2 * tid], w1 = sh.hbm[2 * tid + 1], w2 = (nb == 33) ? sh.hbm[1024] : 0u;
   const uint32_t cnt = __popc(w0) + __popc(w1) + __popc(w2);
   uint32_t* seg = reinterpret_cast<uint32_t*>(a.message + ci.seg_off);
   uint32_t* bm = seg + kSegHeader / 4;
