@@ -743,30 +743,28 @@ __device__ __forceinline__ uint32_t dec_block(uint32_t r, uint32_t t) {
   return t < 256 ? t + 128 : t + 384;
 }
 
-// cA / cB for both CTAs: wb = W_L^b, wn = W_N^b = wb^2
-__device__ __forceinline__ void coefs(float2 wb, float2 wn, float2& a0, float2& a1, float2& b0, float2& b1) {
-  a0 = make_float2(0.5f * (1.0f + wb.y), 0.5f * wb.x);
-  b0 = make_float2(0.5f * (1.0f - wb.y), 0.5f * wb.x);
-  a1 = cmulc(a0, wn);
-  b1 = cmul(b0, wn);
+// Z[k] = ((X[k] + conj X[N-k]) + i t (X[k] - conj X[N-k])) / 2 with t = W_L^-k:
+// the real-IFFT pre-processing (z[n] = x[2n] + i x[2n+1] = IFFT_N(Z)[n]).
+__device__ __forceinline__ float2 zval(float2 a, float2 b, float2 t) {
+  const float2 s = make_float2(a.x + b.x, a.y - b.y);      // a + conj b
+  const float2 d = make_float2(a.x - b.x, a.y + b.y);      // a - conj b
+  const float2 u = cmul(t, d);
+  return make_float2(0.5f * (s.x - u.y), 0.5f * (s.y + u.x));
 }
 
-// Y_0 and Y_1 at m from X[m], X[m+M], X[N-m], X[M-m] with w = W_L^m, w2 = W_N^m.
-__device__ __forceinline__ void y_pair(float2 xm, float2 xmM, float2 xNm, float2 xMm, float2 w, float2 w2,
-                                       float2& y0, float2& y1) {
-  float2 a0, a1, b0, b1;
-  coefs(w, w2, a0, a1, b0, b1);
-  y0 = cmul(a0, xm);
-  y1 = cmul(a1, xm);
-  coefs(make_float2(w.y, -w.x), make_float2(-w2.x, -w2.y), a0, a1, b0, b1);      // b = m + M
-  y0 = cadd(y0, cmul(a0, xmM));
-  y1 = cadd(y1, cmul(a1, xmM));
-  coefs(make_float2(-w.x, w.y), conjf2(w2), a0, a1, b0, b1);                      // b = N - m
-  y0 = cadd(y0, cmul(b0, conjf2(xNm)));
-  y1 = cadd(y1, cmul(b1, conjf2(xNm)));
-  coefs(make_float2(-w.y, -w.x), make_float2(-w2.x, w2.y), a0, a1, b0, b1);       // b = M - m
-  y0 = cadd(y0, cmul(b0, conjf2(xMm)));
-  y1 = cadd(y1, cmul(b1, conjf2(xMm)));
+// Group k -> {Y0[k], Y1[k], Y0[M-k], Y1[M-k]} with Y_r[m] = W_N^-(r m) (Z[m] + (-1)^r Z[m+M]).
+// w = W_L^k; W_L^-(k+M) = i conj w, W_L^-(N-k) = -w, W_L^-(M-k) = i w, W_N^-(M-k) = -w^2.
+__device__ __forceinline__ void y_group(float2 xk, float2 xMk, float2 xkM, float2 xNk, float2 w, float2 (&y)[4]) {
+  const float2 v = conjf2(w);                               // W_L^-k
+  const float2 zk = zval(xk, xNk, v);
+  const float2 zkM = zval(xkM, xMk, make_float2(-v.y, v.x));
+  const float2 zMk = zval(xMk, xkM, make_float2(-w.y, w.x));
+  const float2 zNk = zval(xNk, xk, make_float2(-w.x, -w.y));
+  const float2 w2 = cmul(w, w);                             // W_N^k
+  y[0] = cadd(zk, zkM);
+  y[1] = cmul(conjf2(w2), csub(zk, zkM));
+  y[2] = cadd(zMk, zNk);
+  y[3] = cmul(make_float2(-w2.x, -w2.y), csub(zMk, zNk));
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
@@ -945,20 +943,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       }
     }
     if (k == 0) { xk.y = 0.f; xNk.y = 0.f; }                // imag of DC / Nyquist ignored
-    const float2 w = tw(sh.thi, sh.tlo, k);                 // W_L^k
-    const float2 w2 = cmul(w, w);                           // W_N^k
-    y_pair(xk, xkM, xNk, xMk, w, w2, ys[i][0], ys[i][1]);
-    // m' = M - k: X[m'] = X[M-k], X[m'+M] = X[N-k], X[N-m'] = X[M+k], X[M-m'] = X[k]
-    const float2 wp = make_float2(-w.y, -w.x);              // W_L^(M-k) = -i conj w
-    const float2 w2p = make_float2(-w2.x, w2.y);            // W_N^(M-k) = -conj w2
-    y_pair(xMk, xNk, xkM, xk, wp, w2p, ys[i][2], ys[i][3]);
+    y_group(xk, xMk, xkM, xNk, tw(sh.thi, sh.tlo, k), ys[i]);
   }
   // CTA 1's extra group k = 8192 (m = M - m = 8192): bins 8192 (slot 4096) and 24576 (slot 12288)
   float2 y8192_0 = make_float2(0.f, 0.f), y8192_1 = make_float2(0.f, 0.f);
   if (r == 1 && tid == 0) {
     const float2 x8 = acc[pad(4096u)], x24 = acc[pad(12288u)];
-    const float2 w = tw(sh.thi, sh.tlo, 8192u), w2 = cmul(w, w);
-    y_pair(x8, x24, x24, x8, w, w2, y8192_0, y8192_1);
+    float2 y[4];
+    y_group(x8, x8, x24, x24, tw(sh.thi, sh.tlo, 8192u), y);
+    y8192_0 = y[0];
+    y8192_1 = y[1];
   }
   FGC_TS(3);
   cluster.sync();                                           // all X reads done (both CTAs)

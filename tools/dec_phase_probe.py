@@ -39,7 +39,8 @@ lib.fgc_debug_fused_timestamps(ts.ctypes.data, ts.size)
 nct = min(2048, 2 * (n // 65536))
 t = ts[: nct * 16].reshape(nct, 16).astype(np.int64)
 order = [(0, 7, "msg0 loads+scan"), (7, 8, "msg0-3 codes"), (8, 1, "rest msgs"), (1, 2, "cluster sync 1"),
-         (2, 3, "Y gather+twiddle"), (3, 4, "cluster sync 2"), (4, 5, "ifft pass12"), (5, 6, "pass3+store")]
+         (2, 3, "Y gather+twiddle"), (3, 4, "cluster sync 2"), (4, 9, "Y store+sync 3"), (9, 5, "ifft pass12"),
+         (5, 6, "pass3+store")]
 print(f"W={W} CTA span (TS0->TS6) mean {((t[:, 6] - t[:, 0]) / 1e3).mean():.1f} us")
 for a, b, nm in order:
     d = (t[:, b] - t[:, a]) / 1e3
