@@ -986,6 +986,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   FGC_TS(5);
   const float scale = 1.0f / (float)kN;
   float* out = a.out + ci.in_off;
+  float dbg_sum = 0.f;
   for (uint32_t c = 0; c < 2; ++c) {
     const uint32_t k = tid + 512u * c;
     float2 o[16];
@@ -993,9 +994,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
       const uint32_t p = k + 1024u * m;
-      *reinterpret_cast<float2*>(out + 4ull * p + 2 * r) = make_float2(o[m].x * scale, o[m].y * scale);
+      if (!(dbg & 2u)) *reinterpret_cast<float2*>(out + 4ull * p + 2 * r) = make_float2(o[m].x * scale, o[m].y * scale);
+      else dbg_sum += o[m].x + o[m].y;
     }
   }
+  if (dbg & 2u) out[tid + 512 * r] = dbg_sum;
   FGC_TS(6);
 }
 

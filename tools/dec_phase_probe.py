@@ -30,7 +30,7 @@ dec = lambda: _lib.check(lib.fgc_decode_average(plan.handle, stacked.data_ptr(),
                                                 wt.ctypes.data, out.data_ptr(), D.stream()))
 dec()
 flush.fill_(1.0)
-lib.fgc_debug_set_fused_knobs(128)
+lib.fgc_debug_set_fused_knobs(128 | (int(sys.argv[3]) if len(sys.argv) > 3 else 0))
 dec()
 torch.cuda.synchronize()
 lib.fgc_debug_set_fused_knobs(0)
