@@ -559,3 +559,40 @@ def test_truncate_energy_mode_complex128(n, theta):
     ref[dropped] = False
     np.testing.assert_array_equal(mask, ref)
     np.testing.assert_array_equal(out.coefficients, np.where(mask, c, 0))
+
+
+# ---------------------------------------------------------------- fused-path inputs
+
+def test_fused_input_flags():
+    """The fused load raises the reference's errors (codec.py:213-226) for
+    65536-sample chunks too: non-finite input, binary16 overflow."""
+    rng = np.random.default_rng(21)
+    g = (rng.standard_normal(2 * 65536) * 1e-2).astype(np.float32)
+    q = F.tune_eps(-200.0, 200.0, 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.9), q)
+    bad = g.copy()
+    bad[70000] = np.nan
+    with pytest.raises(ValueError):
+        F.compress(bad, cfg)
+    big = g.copy()
+    big[123] = 1e6                                   # > binary16 max: overflows the half pass
+    with pytest.raises(ValueError, match="binary16"):
+        F.compress(big, F.CodecConfig(F.SparsificationSpec(0.9), q, half_precision_pass=True))
+
+
+def test_fused_half_pass_and_float64_input():
+    """half_precision_pass (spectral.py:189-196) and float64 gradients through
+    the fused kernels: the message equals the oracle's message built from the
+    GPU's own coefficients, and float64 input matches its float32 rounding."""
+    rng = np.random.default_rng(22)
+    n = 3 * 65536 + 1000
+    g64 = rng.standard_normal(n) * 1e-2
+    q = F.calibrate([g64], 8, 3)
+    hcfg = F.CodecConfig(F.SparsificationSpec(0.9), q, half_precision_pass=True)
+    msg = F.compress(g64, hcfg)
+    om = _oracle_message_from_gpu_coeffs(g64, hcfg, n, 65536, 0.9, q)
+    assert F.serialize(msg)[36:] == O.to_wire(om)[36:]    # payloads; the header carries the half flag
+    cfg = F.CodecConfig(F.SparsificationSpec(0.9), q)
+    m64 = F.compress(g64, cfg)
+    m32 = F.compress(g64.astype(np.float32), cfg)
+    assert F.serialize(m64) == F.serialize(m32)
