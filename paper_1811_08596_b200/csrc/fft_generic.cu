@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <algorithm>
+
 #include "fgc_device.cuh"
 #include "fgc_internal.h"
 
@@ -178,37 +180,54 @@ __global__ void k_direct_dft(const typename V2<R>::T* in, typename V2<R>::T* out
 }
 
 // Mixed-radix outer pass, Lc = A * B.  Index n = B n1 + n2, k = k1 + A k2.
-//   forward (dir < 0): Y[k1 B + n2] = sum_n1 x[B n1 + n2] W^(k1 (B n1 + n2))
+//   forward (dir < 0): Y[k1 B + n2] = W^(k1 n2) sum_n1 x[B n1 + n2] W_A^(k1 n1)
 //                      (then a B-point FFT down each row k1 gives X[k1 + A k2])
-//   inverse (dir > 0): x[B n1 + n2] = sum_k1 Y'[k1 B + n2] W^(-k1 (B n1 + n2))
+//   inverse (dir > 0): x[B n1 + n2] = sum_k1 W_A^(-k1 n1) (W^(-k1 n2) Y'[k1 B + n2])
 //                      (after the B-point inverse FFT of each row k1)
-// W = exp(-2 pi i / Lc) from the exact table mtw.  One thread per output.
+// W = exp(-2 pi i / Lc) (exact table mtw), W_A = W^B.  A CTA takes `cols`
+// columns n2 and `kg` output rows: the A x cols input tile (pre-twiddled for
+// the inverse) and the A-entry W_A table sit in shared memory, so the A-term
+// sums read no global memory.
 template <class T2>
-__global__ void k_mixed_pass(const T2* in, T2* out, const T2* mtw, uint32_t A, uint32_t B, uint64_t total, int dir) {
-  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= total) return;
+__global__ void __launch_bounds__(256) k_mixed_pass(const T2* in, T2* out, const T2* mtw, uint32_t A, uint32_t B,
+                                                    uint32_t cols, uint32_t kg, int dir) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T2* wa = reinterpret_cast<T2*>(smraw);              // W_A^m (conjugated for the inverse), m < A
+  T2* tile = wa + A;                                  // [A][cols]
   const uint32_t Lc = A * B;
-  const uint64_t item = e / Lc;
-  const uint32_t r = (uint32_t)(e - item * Lc);
-  const uint32_t o = r / B, n2 = r - o * B;         // o = k1 (forward) or n1 (inverse)
-  const T2* src = in + item * Lc + n2;
-  uint32_t m, step;
-  if (dir < 0) {                                     // m = o (B i + n2)
-    m = (uint32_t)(((uint64_t)o * n2) % Lc);
-    step = (uint32_t)(((uint64_t)o * B) % Lc);
-  } else {                                           // m = i (B o + n2)
-    m = 0;
-    step = o * B + n2;
-  }
-  T2 acc = mk(src[0].x * 0, src[0].y * 0);
-  for (uint32_t i = 0; i < A; ++i) {
-    T2 w = mtw[m];
+  const uint64_t item = blockIdx.z;
+  const uint32_t c0 = blockIdx.x * cols, nc = min(cols, B - c0);
+  const uint32_t o0 = blockIdx.y * kg, no = min(kg, A - o0);
+  const T2* src = in + item * Lc;
+  for (uint32_t m = threadIdx.x; m < A; m += blockDim.x) {
+    T2 w = mtw[(uint64_t)m * B];
     if (dir > 0) w.y = -w.y;
-    acc = zadd(acc, zmul(src[(uint64_t)i * B], w));
-    m += step;
-    if (m >= Lc) m -= Lc;
+    wa[m] = w;
   }
-  out[e] = acc;
+  for (uint32_t e = threadIdx.x; e < A * nc; e += blockDim.x) {
+    const uint32_t i = e / nc, c = e - i * nc;
+    T2 v = src[(uint64_t)i * B + c0 + c];
+    if (dir > 0) {                                    // W^(-i n2)
+      T2 w = mtw[((uint64_t)i * (c0 + c)) % Lc];
+      w.y = -w.y;
+      v = zmul(v, w);
+    }
+    tile[i * cols + c] = v;
+  }
+  __syncthreads();
+  T2* dst = out + item * Lc;
+  for (uint32_t e = threadIdx.x; e < no * nc; e += blockDim.x) {
+    const uint32_t ol = e / nc, c = e - ol * nc, o = o0 + ol;
+    T2 acc = mk(tile[0].x * 0, tile[0].y * 0);
+    uint32_t m = 0;
+    for (uint32_t i = 0; i < A; ++i) {
+      acc = zadd(acc, zmul(tile[i * cols + c], wa[m]));
+      m += o;
+      if (m >= A) m -= A;
+    }
+    if (dir < 0) acc = zmul(acc, mtw[((uint64_t)o * (c0 + c)) % Lc]);   // W^(k1 n2)
+    dst[(uint64_t)o * B + c0 + c] = acc;
+  }
 }
 
 template <class T2>
@@ -221,13 +240,37 @@ __global__ void k_pointwise_mul(T2* data, const T2* f, uint32_t P, uint64_t tota
 inline uint32_t ceil_div(uint64_t a, uint32_t b) { return (uint32_t)((a + b - 1) / b); }
 
 template <class R>
+fgc_status mixed_pass(const typename V2<R>::T* in, typename V2<R>::T* out, const typename V2<R>::T* mtw, uint32_t A,
+                      uint32_t B, uint32_t batch, int dir, cudaStream_t s) {
+  using T2 = typename V2<R>::T;
+  // columns per CTA: up to 32, within ~96 KB of tile; rows so a CTA has ~256 outputs
+  uint32_t cols = 32;
+  while (cols > 1 && (uint64_t)(A + A * cols) * sizeof(T2) > 96 * 1024) cols >>= 1;
+  cols = std::min(cols, B);
+  const uint32_t kg = std::max(1u, 256u / cols);
+  const size_t smem = (size_t)(A + A * cols) * sizeof(T2);
+  static bool attr = false;
+  if (!attr) {
+    FGC_CUDA(cudaFuncSetAttribute(k_mixed_pass<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    FGC_CUDA(cudaFuncSetAttribute(k_mixed_pass<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    attr = true;
+  }
+  const dim3 grid(ceil_div(B, cols), ceil_div(A, kg), batch);
+  k_mixed_pass<T2><<<grid, 256, smem, s>>>(in, out, mtw, A, B, cols, kg, dir);
+  FGC_LAUNCHED(1);
+  return FGC_OK;
+}
+
+template <class R>
 fgc_status pow2_rec(typename V2<R>::T* data, uint64_t batch, uint32_t P, const typename V2<R>::T* tw, uint32_t twP,
                     int dir, cudaStream_t s) {
   using T2 = typename V2<R>::T;
   if (P <= 1 || batch == 0) return FGC_OK;
   const uint32_t cap = smem_points(sizeof(R));   // points per CTA, held twice in 64 KB
   if (P <= cap) {
-    const uint32_t per = max(1u, cap / P);
+    // transforms per CTA: up to a full shared-memory tile, but small batches
+    // are spread over the SMs (latency, not throughput, rules there)
+    const uint32_t per = max(1u, min(cap / P, (uint32_t)((batch + 295) / 296)));
     const size_t smem = 2ull * per * P * sizeof(T2);
     k_smem_fft<T2><<<ceil_div(batch, per), kFftThreads, smem, s>>>(data, P, per, batch, tw, twP, dir);
     FGC_LAUNCHED(1);
@@ -352,18 +395,12 @@ fgc_status DftPlanT<R>::run(int dir, DftResultT<R>& res, cudaStream_t s) {
     case DftKind::Mixed: {
       const uint64_t total = (uint64_t)batch * Lc;
       if (dir < 0) {                                 // natural work -> rows in work2 (engine layout)
-        if (total) {
-          k_mixed_pass<T2><<<ceil_div(total, 256), 256, 0, s>>>(work, work2, mtw, A, B, total, -1);
-          FGC_LAUNCHED(1);
-        }
+        if (total) FGC_TRY(mixed_pass<R>(work, work2, mtw, A, B, batch, -1, s));
         FGC_TRY(pow2_rec<R>(work2, (uint64_t)batch * A, B, tw, B, -1, s));
         res = DftResultT<R>{work2, Lc, 2, 0};
       } else {                                       // rows (engine layout) in work -> natural work2
         FGC_TRY(pow2_rec<R>(work, (uint64_t)batch * A, B, tw, B, +1, s));
-        if (total) {
-          k_mixed_pass<T2><<<ceil_div(total, 256), 256, 0, s>>>(work, work2, mtw, A, B, total, +1);
-          FGC_LAUNCHED(1);
-        }
+        if (total) FGC_TRY(mixed_pass<R>(work, work2, mtw, A, B, batch, +1, s));
         res = DftResultT<R>{work2, Lc, 0, 0};
       }
       return FGC_OK;
