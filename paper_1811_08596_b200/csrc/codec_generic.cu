@@ -55,6 +55,26 @@ struct Coeffs<double2> {
   }
 };
 
+// Visit every bin of the chunk, each thread 4 bins per round with their loads
+// issued together (the passes are latency-bound on these loads otherwise).
+template <typename CT, typename F>
+__device__ __forceinline__ void for_bins(const Coeffs<CT>& cf, uint32_t B, F&& f) {
+  for (uint32_t i0 = threadIdx.x; i0 < B; i0 += 4 * kSelThreads) {
+    float re[4], im[4];
+    double dr[4], di[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * kSelThreads;
+      if (i < B) cf.get(i, re[u], im[u], dr[u], di[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * kSelThreads;
+      if (i < B) f(i, re[u], im[u], dr[u], di[u]);
+    }
+  }
+}
+
 // Bucket b such that below(b) <= r < below(b) + hist[b]; every thread returns it.
 __device__ void find_bucket(SelectShared& sh, uint32_t r, uint32_t& bucket, uint32_t& below) {
   constexpr uint32_t per = kHistBins / kSelThreads;   // 4
@@ -144,23 +164,19 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
       // pass 1: proxy bits [30:20]
       for (uint32_t b = tid; b < kHistBins; b += kSelThreads) sh.hist[b] = 0;
       __syncthreads();
-      for (uint32_t i = tid; i < B; i += kSelThreads) {
-        float re, im; double dr, di;
-        cf.get(i, re, im, dr, di);
+      for_bins(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
         atomicAdd(&sh.hist[__float_as_uint(proxy_key(re, im)) >> 20], 1u);
-      }
+      });
       __syncthreads();
       uint32_t b1, below1;
       find_bucket(sh, r, b1, below1);
       // pass 2: proxy bits [19:9] inside bucket b1
       for (uint32_t b = tid; b < kHistBins; b += kSelThreads) sh.hist[b] = 0;
       __syncthreads();
-      for (uint32_t i = tid; i < B; i += kSelThreads) {
-        float re, im; double dr, di;
-        cf.get(i, re, im, dr, di);
+      for_bins(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
         const uint32_t pb = __float_as_uint(proxy_key(re, im));
         if ((pb >> 20) == b1) atomicAdd(&sh.hist[(pb >> 9) & 0x7FFu], 1u);
-      }
+      });
       __syncthreads();
       uint32_t b2, below2;
       find_bucket(sh, r - below1, b2, below2);
@@ -178,9 +194,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
     if (tid == 0) sh.cnt = 0;
     __syncthreads();
     uint32_t below_local = 0;
-    for (uint32_t i = tid; i < B; i += kSelThreads) {
-      float re, im; double dr, di;
-      cf.get(i, re, im, dr, di);
+    for_bins(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
       const float p = proxy_key(re, im);
       if (!all_band && p < band_lo) {
         ++below_local;
@@ -188,7 +202,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
         const uint32_t s = atomicAdd(&sh.cnt, 1u);
         if (s < kCandCap) sh.idx[s] = i;
       }
-    }
+    });
     const uint32_t below = block_sum<kSelThreads>(below_local, sh.scan);
     m = sh.cnt;
     need = kdrop - below;
@@ -223,14 +237,12 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
           for (uint32_t b = tid; b < kHistBins; b += kSelThreads) sh.hist[b] = 0;
           __syncthreads();
           const unsigned long long dm = (1ull << widths[pass]) - 1ull;
-          for (uint32_t i = tid; i < B; i += kSelThreads) {
-            float re, im; double dr, di;
-            cf.get(i, re, im, dr, di);
+          for_bins(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
             const float p = proxy_key(re, im);
-            if (!(all_band || (p >= band_lo && p < band_hi))) continue;
+            if (!(all_band || (p >= band_lo && p < band_hi))) return;
             const unsigned long long key = (unsigned long long)__double_as_longlong(cabs_key(dr, di));
             if ((key & pmask) == prefix) atomicAdd(&sh.hist[(key >> shifts[pass]) & dm], 1u);
-          }
+          });
           __syncthreads();
           uint32_t bk, bl;
           find_bucket(sh, rr, bk, bl);
@@ -259,11 +271,14 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
   for (uint32_t s = tid; s < stage_words; s += kSelThreads) sh.stage[s] = 0;
   __syncthreads();
 
+  float nre = 0.f, nim = 0.f; double ndr = 0.0, ndi = 0.0;   // the next tile's bin, loaded a tile ahead
+  if (tid < B) cf.get(tid, nre, nim, ndr, ndi);
   for (uint32_t t0 = 0; t0 < B; t0 += kSelThreads) {
     const uint32_t i = t0 + tid;
     const bool valid = i < B;
-    float re = 0.f, im = 0.f; double dr = 0.0, di = 0.0;
-    if (valid) cf.get(i, re, im, dr, di);
+    const float re = nre, im = nim;
+    const double dr = ndr, di = ndi;
+    if (i + kSelThreads < B) cf.get(i + kSelThreads, nre, nim, ndr, ndi);
     bool dropped = false;
     bool is_tie = false;
     unsigned long long key = 0;

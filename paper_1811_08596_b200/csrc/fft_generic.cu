@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(256) k_mixed_pass(const T2* in, T2* out, const
   for (uint32_t e = threadIdx.x; e < A * nc; e += blockDim.x) {
     const uint32_t i = e / nc, c = e - i * nc;
     T2 v = src[(uint64_t)i * B + c0 + c];
-    if (dir > 0) {                                    // W^(-i n2)
-      T2 w = mtw[((uint64_t)i * (c0 + c)) % Lc];
+    if (dir > 0) {                                    // W^(-i n2); i n2 < 2^32 since Lc < 2^31
+      T2 w = mtw[(uint32_t)(((uint64_t)i * (c0 + c)) % Lc)];
       w.y = -w.y;
       v = zmul(v, w);
     }
@@ -218,15 +218,28 @@ __global__ void __launch_bounds__(256) k_mixed_pass(const T2* in, T2* out, const
   T2* dst = out + item * Lc;
   for (uint32_t e = threadIdx.x; e < no * nc; e += blockDim.x) {
     const uint32_t ol = e / nc, c = e - ol * nc, o = o0 + ol;
-    T2 acc = mk(tile[0].x * 0, tile[0].y * 0);
+    // four independent partial sums (i mod 4) shorten the dependency chain
+    T2 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = mk(tile[0].x * 0, tile[0].y * 0);
     uint32_t m = 0;
-    for (uint32_t i = 0; i < A; ++i) {
-      acc = zadd(acc, zmul(tile[i * cols + c], wa[m]));
+    uint32_t i = 0;
+    for (; i + 4 <= A; i += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc[u] = zadd(acc[u], zmul(tile[(i + u) * cols + c], wa[m]));
+        m += o;
+        if (m >= A) m -= A;
+      }
+    }
+    for (; i < A; ++i) {
+      acc[0] = zadd(acc[0], zmul(tile[i * cols + c], wa[m]));
       m += o;
       if (m >= A) m -= A;
     }
-    if (dir < 0) acc = zmul(acc, mtw[((uint64_t)o * (c0 + c)) % Lc]);   // W^(k1 n2)
-    dst[(uint64_t)o * B + c0 + c] = acc;
+    T2 sum = zadd(zadd(acc[0], acc[1]), zadd(acc[2], acc[3]));
+    if (dir < 0) sum = zmul(sum, mtw[(uint32_t)(((uint64_t)o * (c0 + c)) % Lc)]);   // W^(k1 n2)
+    dst[(uint64_t)o * B + c0 + c] = sum;
   }
 }
 
@@ -247,7 +260,8 @@ fgc_status mixed_pass(const typename V2<R>::T* in, typename V2<R>::T* out, const
   uint32_t cols = 32;
   while (cols > 1 && (uint64_t)(A + A * cols) * sizeof(T2) > 96 * 1024) cols >>= 1;
   cols = std::min(cols, B);
-  const uint32_t kg = std::max(1u, 256u / cols);
+  // ~64 outputs per CTA: the A-term sums are latency-bound, so spread them wide
+  const uint32_t kg = std::max(1u, 64u / cols);
   const size_t smem = (size_t)(A + A * cols) * sizeof(T2);
   static bool attr = false;
   if (!attr) {
