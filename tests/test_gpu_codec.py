@@ -596,3 +596,35 @@ def test_fused_half_pass_and_float64_input():
     m64 = F.compress(g64, cfg)
     m32 = F.compress(g64.astype(np.float32), cfg)
     assert F.serialize(m64) == F.serialize(m32)
+
+
+# ---------------------------------------------------------------- randomized parity sweep
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("FGC_SWEEP", "16"))))
+def test_random_configs_match_oracle(seed):
+    """Random lengths, chunk sizes (powers of two, odd, mixed-radix and prime
+    tails), keep ratios, lattices and modes: the message built from the GPU's
+    own coefficients is byte-identical to the oracle's, and decompression
+    matches the oracle's to 1e-5."""
+    rng = np.random.default_rng(1000 + seed)
+    chunk = int(rng.choice([16, 17, 100, 1024, 4096, 5000, 65536]))
+    n = int(rng.integers(1, 4)) * chunk + int(rng.integers(0, chunk))
+    theta = float(rng.choice([0.0, 0.25, 0.5, 0.9, 0.97, 1.0]))
+    nm = [(8, 3), (4, 2), (6, 2), (16, 9), None][int(rng.integers(0, 5))]
+    mode = "energy" if rng.random() < 0.3 else "count"
+    g = (rng.standard_normal(n) * 10.0 ** rng.uniform(-4, 1)).astype(np.float32)
+    q = None if nm is None else F.calibrate([g], *nm)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta, mode), q, chunk_size=chunk)
+    spec = debug.forward_spectrum(g, cfg)
+    msg = F.compress(g, cfg)
+    chunks, pos = [], 0
+    for L in O.chunk_lengths(n, chunk):
+        b = L // 2 + 1
+        chunks.append(O.encode_spectrum(spec[pos:pos + b], L, theta, mode, lat_of(q))[1])
+        pos += b
+    om = O.Message(n, chunk, float(np.float32(theta)), mode, False, lat_of(q), chunks)
+    assert F.serialize(msg) == O.to_wire(om), (n, chunk, theta, nm, mode)
+    ref = O.decompress(om)
+    got = F.decompress(msg)
+    scale = max(np.abs(ref).max(), 1e-30)
+    assert np.abs(got - ref).max() <= 1e-5 * scale, (n, chunk, theta, nm, mode)
