@@ -315,6 +315,16 @@ fgc_status fgc_exchange_message(fgc_exchange* x, int parity, uint8_t** message, 
 fgc_status fgc_exchange_average(fgc_plan* plan, fgc_exchange* x, const void* grad, int dtype,
                                 const double* weights, float* out, uint32_t* flags, void* stream);
 
+/* The averaging step from and to HOST memory (pinned for overlap): the
+ * host->device copy of the gradient and the device->host copy of the
+ * average run on copy streams in pieces of consecutive chunks, overlapped
+ * with the codec kernels.  x = NULL: single rank (message is this rank's
+ * device message buffer); otherwise the peer exchange (message ignored).
+ * dev_grad (n values of dtype) and dev_out (n floats) are device scratch. */
+fgc_status fgc_average_host(fgc_plan* plan, fgc_exchange* x, const void* host_grad, int dtype,
+                            const double* weights, void* dev_grad, uint8_t* message, float* dev_out,
+                            float* host_out, uint32_t* flags, void* stream);
+
 /* ---- misc -------------------------------------------------------------- */
 const char* fgc_last_error(void);   /* thread-local message of the last failure */
 int         fgc_version(void);      /* 0xMMmmpp                                  */

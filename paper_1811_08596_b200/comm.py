@@ -201,6 +201,39 @@ class GradientAverager:
                                                   D.stream()))
         return dst
 
+    def step_host(self, grad: torch.Tensor, out: torch.Tensor | None = None, wait: bool = True) -> torch.Tensor:
+        """The averaging step from and to host memory: the PCIe copies of the
+        gradient and of the average overlap the codec kernels piece by piece
+        (fgc_average_host).  Pass pinned CPU tensors for the overlap.  With
+        wait=False the call returns once the work is queued on the current
+        stream; synchronize it before reading `out`."""
+        if grad.numel() != self.n or grad.is_cuda:
+            raise ValueError("gradient must be a host tensor of the planned length")
+        if grad.dtype not in (torch.float32, torch.float64):
+            raise ValueError("gradient must be float32 or float64")
+        code = _lib.DTYPE_F64 if grad.dtype == torch.float64 else _lib.DTYPE_F32
+        grad = grad.contiguous()
+        dst = out if out is not None else torch.empty(self.n, dtype=torch.float32, pin_memory=True)
+        if dst.is_cuda or dst.numel() != self.n or dst.dtype != torch.float32:
+            raise ValueError("out must be a float32 host tensor of the planned length")
+        dg = getattr(self, "_dgrad", None)
+        if dg is None or dg.dtype != grad.dtype:
+            dg = self._dgrad = torch.empty(self.n, dtype=grad.dtype, device=self.out.device)
+        if self.world > 1 and self.exchange is None:
+            # NCCL transport: plain copies around the device step
+            dg.copy_(grad, non_blocking=True)
+            dst.copy_(self.step(dg), non_blocking=True)
+            if wait:
+                torch.cuda.current_stream().synchronize()
+            return dst
+        x = self.exchange.handle if self.exchange is not None else None
+        _lib.check(_lib.lib.fgc_average_host(self.plan.handle, x, grad.data_ptr(), code, self.weights.ctypes.data,
+                                             dg.data_ptr(), self.message.data_ptr(), self.out.data_ptr(),
+                                             dst.data_ptr(), self.flags.data_ptr(), D.stream()))
+        if wait:
+            torch.cuda.current_stream().synchronize()
+        return dst
+
     def check(self) -> None:
         """Raise the reference's ValueError if any step saw a bad gradient."""
         f = D.read_flags(self.flags)

@@ -224,7 +224,7 @@ fgc_status launch_fused_inverse(const FusedTables* t, const ChunkInfo* d_chunks,
 
 // Peer exchange internals (xchg.cu).
 fgc_status exchange_publish_event(fgc_exchange* x, int k, uint64_t lo, uint64_t bytes, cudaEvent_t ready,
-                                  uint32_t value);
+                                  uint32_t value, int fi = -1);
 fgc_status exchange_publish_piece(fgc_exchange* x, int k, uint32_t i, uint64_t lo, uint64_t bytes,
                                   uint32_t count_target, uint32_t value);
 fgc_status exchange_wait(fgc_exchange* x, cudaStream_t s, int fi, uint32_t value);

@@ -51,6 +51,10 @@ struct fgc_plan {
   FusedTables* fused = nullptr;
   uint32_t fused_first = 0, fused_count = 0;     // chunk range taken by fused kernels
   EnergyScratch energy;              // energy-mode selection scratch (allocated on first use)
+  // host-buffer averaging: copy streams and per-piece events (created on first use)
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> ev_h, ev_c2, ev_d;
+  cudaEvent_t ev_step = nullptr;
   // pipelined allgather-average: exchange stream + per-piece events (created on first use)
   cudaStream_t xstream = nullptr;
   std::vector<cudaEvent_t> ev_comp, ev_gath;
@@ -248,6 +252,12 @@ extern "C" void fgc_plan_destroy(fgc_plan* p) {
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->side) cudaStreamDestroy(p->side);
+  for (cudaEvent_t e : p->ev_h) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_c2) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_d) cudaEventDestroy(e);
+  if (p->ev_step) cudaEventDestroy(p->ev_step);
+  if (p->h2d) cudaStreamDestroy(p->h2d);
+  if (p->d2h) cudaStreamDestroy(p->d2h);
   for (cudaEvent_t e : p->ev_comp) cudaEventDestroy(e);
   for (cudaEvent_t e : p->ev_gath) cudaEventDestroy(e);
   if (p->xstream) cudaStreamDestroy(p->xstream);
@@ -762,6 +772,157 @@ extern "C" fgc_status fgc_exchange_average(fgc_plan* p, fgc_exchange* x, const v
   exchange_trace(s, "end");
   *step += 1;
   (void)counter;
+  return FGC_OK;
+}
+
+// Averaging step from and to HOST buffers: the PCIe transfers overlap the
+// codec in pieces of consecutive chunks.  Piece i's host->device copy runs on
+// a copy stream while piece i-1 compresses; piece i decodes as soon as it is
+// compressed (W = 1) or its exchange landed (peer exchange), and its
+// device->host copy overlaps the next pieces.  The generic (tail) chunks are
+// copied in first and run their longer kernel chain on the side stream, off
+// the critical path of the last piece.
+extern "C" fgc_status fgc_average_host(fgc_plan* p, fgc_exchange* x, const void* host_grad, int dtype,
+                                       const double* weights, void* dev_grad, uint8_t* message, float* dev_out,
+                                       float* host_out, uint32_t* flags, void* stream) {
+  if (!p || !host_grad || !dev_grad || !dev_out || !host_out || !flags) {
+    set_error("null argument");
+    return FGC_ERR_INVALID;
+  }
+  if (dtype != FGC_DTYPE_F32 && dtype != FGC_DTYPE_F64) { set_error("unknown dtype"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_mode(p));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int W = 1, me = 0;
+  uint32_t* counter = nullptr;
+  uint64_t* step = nullptr;
+  uint64_t mb = p->msg_bytes;
+  if (x) {
+    if (!exchange_ready(x)) { set_error("exchange not opened"); return FGC_ERR_INVALID; }
+    exchange_counters(x, &counter, &step, &W, &me, &mb);
+    if (mb != p->msg_bytes) { set_error("exchange sized for another plan"); return FGC_ERR_INVALID; }
+  } else if (!message) {
+    set_error("single-rank host averaging needs a message buffer");
+    return FGC_ERR_INVALID;
+  }
+  Weights w;
+  FGC_TRY(fill_weights(weights, W, w));
+  const uint32_t Pmax = exchange_max_pieces();
+  const bool energy = p->desc.mode == FGC_MODE_ENERGY;
+  uint32_t P = 8;
+  if (const char* e = getenv("FGC_HOST_PIECES")) P = (uint32_t)std::max(1, atoi(e));
+  P = (energy || !p->fused_count) ? 0 : std::min(std::min(P, Pmax), p->fused_count);
+  if (!p->h2d) {
+    FGC_CUDA(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
+    FGC_CUDA(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
+    FGC_CUDA(cudaEventCreateWithFlags(&p->ev_step, cudaEventDisableTiming));
+  }
+  while (p->ev_h.size() < P + 1) {
+    cudaEvent_t a, b, c;
+    FGC_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    FGC_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    FGC_CUDA(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+    p->ev_h.push_back(a);
+    p->ev_c2.push_back(b);
+    p->ev_d.push_back(c);
+  }
+  int k = 0;
+  uint32_t tval = 0;
+  uint8_t* gathered = message;
+  if (x) {
+    k = (int)(*step & 1);
+    tval = (uint32_t)(*step + 1);
+    FGC_TRY(fgc_exchange_message(x, k, &message, &gathered));
+  }
+  const size_t esz = dtype == FGC_DTYPE_F64 ? 8 : 4;
+  auto h2d = [&](uint64_t lo, uint64_t hi) {
+    return cudaMemcpyAsync(static_cast<uint8_t*>(dev_grad) + lo * esz, static_cast<const uint8_t*>(host_grad) + lo * esz,
+                           (hi - lo) * esz, cudaMemcpyHostToDevice, p->h2d);
+  };
+  auto d2h = [&](uint64_t lo, uint64_t hi) {
+    return cudaMemcpyAsync(host_out + lo, dev_out + lo, (hi - lo) * sizeof(float), cudaMemcpyDeviceToHost, p->d2h);
+  };
+  // the copy streams reuse dev_grad / dev_out only after the work already on s
+  FGC_CUDA(cudaEventRecord(p->ev_step, s));
+  FGC_CUDA(cudaStreamWaitEvent(p->h2d, p->ev_step, 0));
+  FGC_CUDA(cudaStreamWaitEvent(p->d2h, p->ev_step, 0));
+
+  // generic chunks (all of them for energy mode / plans without fused
+  // chunks): elements [g_lo, n), message bytes [m_lo, end), slot P (tail slot
+  // of the exchange)
+  const bool generic = p->classes.size() > (p->fused_count ? 1u : 0u);
+  const uint64_t g_lo = p->fused_count ? p->chunks[p->fused_first + p->fused_count - 1].in_off +
+                                             p->chunks[p->fused_first + p->fused_count - 1].len
+                                       : 0;
+  const uint64_t m_lo = p->fused_count ? p->seg_off[p->fused_first + p->fused_count] : 0;
+  cudaStream_t g = P ? p->side : s;
+  if (generic) {
+    FGC_CUDA(h2d(g_lo, p->desc.n));
+    FGC_CUDA(cudaEventRecord(p->ev_h[P], p->h2d));
+    FGC_CUDA(cudaStreamWaitEvent(g, p->ev_h[P], 0));
+    if (energy) FGC_TRY(energy_compress(p, dev_grad, dtype, nullptr, message, nullptr, flags, g));
+    else FGC_TRY(compress_range(p, dev_grad, dtype, message, flags, g, 0, 0, true));
+    if (x) {
+      FGC_CUDA(cudaEventRecord(p->ev_c2[P], g));
+      FGC_TRY(exchange_publish_event(x, k, m_lo, p->msg_bytes - m_lo, p->ev_c2[P], tval, (int)Pmax));
+      FGC_TRY(exchange_wait(x, g, (int)Pmax, tval));
+    }
+    FGC_TRY(decode_range(p, gathered, W, p->msg_bytes, w, dev_out, g, 0, 0, true));
+    FGC_CUDA(cudaEventRecord(p->ev_d[P], g));
+  }
+  // fused pieces: elements [chunk f[i] .. chunk f[i+1])
+  std::vector<uint32_t> f(P + 1);
+  // half-size first and last pieces: shorter pipeline fill (first copy-in)
+  // and drain (last copy-out)
+  const bool ramp = P >= 3 && p->fused_count >= 2 * P && !getenv("FGC_HOST_NO_RAMP");
+  for (uint32_t i = 0; i <= P; ++i) {
+    const uint64_t u = ramp ? (i == 0 ? 0 : i == P ? 2 * P - 2 : 2 * i - 1) : i;     // in half-pieces
+    const uint64_t un = ramp ? 2 * P - 2 : (P ? P : 1);
+    f[i] = p->fused_first + (uint32_t)((uint64_t)p->fused_count * u / un);
+  }
+  auto elem_lo = [&](uint32_t i) -> uint64_t { return p->chunks[f[i]].in_off; };
+  auto elem_hi = [&](uint32_t i) -> uint64_t { return i + 1 == P ? g_lo : p->chunks[f[i + 1]].in_off; };
+  auto seg_hi = [&](uint32_t i) -> uint64_t { return i + 1 == P ? m_lo : p->seg_off[f[i + 1]]; };
+  for (uint32_t i = 0; i < P; ++i) {
+    FGC_CUDA(h2d(elem_lo(i), elem_hi(i)));
+    FGC_CUDA(cudaEventRecord(p->ev_h[i], p->h2d));
+  }
+  for (uint32_t i = 0; i < P; ++i) {
+    FGC_CUDA(cudaStreamWaitEvent(s, p->ev_h[i], 0));
+    FGC_TRY(compress_range(p, dev_grad, dtype, message, flags, s, f[i], f[i + 1] - f[i], false));
+    if (x) {
+      FGC_CUDA(cudaEventRecord(p->ev_c2[i], s));
+      FGC_TRY(exchange_publish_event(x, k, p->seg_off[f[i]], seg_hi(i) - p->seg_off[f[i]], p->ev_c2[i], tval,
+                                     (int)i));
+    } else {
+      // W = 1: decode this piece right away so its copy-out overlaps the next pieces
+      FGC_TRY(decode_range(p, message, 1, p->msg_bytes, w, dev_out, s, f[i], f[i + 1] - f[i], false));
+      FGC_CUDA(cudaEventRecord(p->ev_d[i], s));
+    }
+  }
+  if (x) {
+    for (uint32_t i = 0; i < P; ++i) {
+      FGC_TRY(exchange_wait(x, s, (int)i, tval));
+      FGC_TRY(decode_range(p, gathered, W, p->msg_bytes, w, dev_out, s, f[i], f[i + 1] - f[i], false));
+      FGC_CUDA(cudaEventRecord(p->ev_d[i], s));
+    }
+  }
+  // copy-out in completion order: the generic chunks finish first
+  if (generic) {
+    FGC_CUDA(cudaStreamWaitEvent(p->d2h, p->ev_d[P], 0));
+    FGC_CUDA(d2h(g_lo, p->desc.n));
+  }
+  for (uint32_t i = 0; i < P; ++i) {
+    FGC_CUDA(cudaStreamWaitEvent(p->d2h, p->ev_d[i], 0));
+    FGC_CUDA(d2h(elem_lo(i), elem_hi(i)));
+  }
+  FGC_CUDA(cudaEventRecord(p->ev_step, p->d2h));
+  FGC_CUDA(cudaStreamWaitEvent(s, p->ev_step, 0));
+  if (x) {
+    FGC_TRY(exchange_join(x, s));
+    *step += 1;
+  }
+  (void)counter;
+  (void)me;
   return FGC_OK;
 }
 

@@ -246,12 +246,14 @@ static fgc_status push(fgc_exchange* x, cudaStream_t cs, int k, uint64_t lo, uin
   return FGC_OK;
 }
 
-// Generic (tail) chunks: push after `ready` (an event on the producing stream).
+// Push after `ready` (an event on the producing stream) and set flag `fi`
+// (default: the generic-chunk slot).
 fgc_status exchange_publish_event(fgc_exchange* x, int k, uint64_t lo, uint64_t bytes, cudaEvent_t ready,
-                                  uint32_t value) {
-  cudaStream_t cs = x->cs[1][0];
+                                  uint32_t value, int fi) {
+  if (fi < 0) fi = kMaxPieces;
+  cudaStream_t cs = x->cs[1][fi % kCopyStreams];
   XC(cudaStreamWaitEvent(cs, ready, 0));
-  return push(x, cs, k, lo, bytes, kMaxPieces, value);
+  return push(x, cs, k, lo, bytes, fi, value);
 }
 
 // Fused piece i: the copy stream waits (stream memory operation) until the

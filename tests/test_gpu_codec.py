@@ -628,3 +628,27 @@ def test_random_configs_match_oracle(seed):
     got = F.decompress(msg)
     scale = max(np.abs(ref).max(), 1e-30)
     assert np.abs(got - ref).max() <= 1e-5 * scale, (n, chunk, theta, nm, mode)
+
+
+# ---------------------------------------------------------------- host-buffer step
+@pytest.mark.parametrize("n,mode,dt", [(8 * 65536, "count", torch.float32), (20 * 65536 + 12345, "count", torch.float32),
+                                       (3 * 65536 + 7, "count", torch.float64), (40000, "count", torch.float32),
+                                       (5 * 65536 + 99, "energy", torch.float32)])
+def test_step_host_matches_device_step(n, mode, dt):
+    """fgc_average_host (PCIe copies overlapped with the codec in pieces)
+    returns the same bits as the device step followed by a plain copy."""
+    from paper_1811_08596_b200.comm import GradientAverager
+    rng = np.random.default_rng(n)
+    g = (rng.standard_normal(n) * 1e-2).astype(np.float64 if dt == torch.float64 else np.float32)
+    q = F.calibrate([g], 8, 3)
+    avg = GradientAverager(n, F.CodecConfig(F.SparsificationSpec(0.9, mode), q), [1.0])
+    ref = avg.step(torch.from_numpy(g).cuda()).cpu()
+    hin = torch.from_numpy(g).pin_memory()
+    hout = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    for _ in range(3):
+        hout.fill_(float("nan"))
+        got = avg.step_host(hin, hout)
+        assert torch.equal(got, ref)
+    avg.check()
+    want = O.decompress(O.from_wire(F.serialize(F.compress(g, avg.config))))
+    assert rel_l2(ref.double().numpy(), want) <= 1e-5

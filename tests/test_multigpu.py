@@ -46,6 +46,11 @@ def _worker(rank, world, port, n, transport, mode, out_q):
         outs = []
         for _ in range(3):                      # the peer exchange alternates two gather buffers
             outs.append(avg.step(g).clone())
+        hin = torch.from_numpy(rows[rank]).pin_memory()
+        for _ in range(2):                      # host-buffer step: same bits as the device step
+            hout = avg.step_host(hin)
+            assert torch.equal(hout, outs[0].cpu()), "host step disagrees"
+            outs.append(avg.step(g).clone())
         avg.check()
         got = outs[0].double().cpu().numpy()
         for o in outs[1:]:
