@@ -244,6 +244,8 @@ def run_ours(args, wl, rank, world, local_rank):
     step_ms = np.array([e[0].elapsed_time(e[1]) for e in step_ev])
     # (2) stage breakdown (not pipelined): compress | allgather | decode-average
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for _ in range(2):                          # NCCL communicator set-up stays out of the stage times
+        one_step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
     barrier()
     for i in range(args.steps):
         flush.fill_(float(i))

@@ -231,6 +231,7 @@ fgc_status exchange_wait(fgc_exchange* x, cudaStream_t s, int fi, uint32_t value
 PieceCounter exchange_counter(fgc_exchange* x, uint32_t first, uint32_t per);
 PieceWait exchange_piece_wait(fgc_exchange* x, uint32_t first, uint32_t per, uint32_t target);
 uint32_t exchange_max_pieces();
+uint32_t exchange_piece_target(fgc_exchange* x, uint32_t i, uint32_t chunks);
 fgc_status exchange_join(fgc_exchange* x, cudaStream_t s);
 fgc_status exchange_events(fgc_exchange* x, uint32_t P, std::vector<cudaEvent_t>** ev);
 void exchange_counters(fgc_exchange* x, uint32_t** counter, uint64_t** step, int* nranks, int* rank,

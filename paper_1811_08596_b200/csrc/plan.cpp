@@ -760,7 +760,7 @@ extern "C" fgc_status fgc_exchange_average(fgc_plan* p, fgc_exchange* x, const v
     for (uint32_t i = 0; i < P; ++i) {
       const uint32_t c0 = p->fused_first + i * per, c1 = std::min(p->fused_first + p->fused_count, c0 + per);
       const uint64_t lo = p->seg_off[c0], hi = p->seg_off[c1];
-      FGC_TRY(exchange_publish_piece(x, k, i, lo, hi - lo, (uint32_t)((*step + 1) * (c1 - c0)), tval));
+      FGC_TRY(exchange_publish_piece(x, k, i, lo, hi - lo, exchange_piece_target(x, i, c1 - c0), tval));
     }
     // one decode launch; each chunk's CTAs wait for their piece from every peer
     FGC_TRY(launch_fused_decode(p->fused, p->d_chunks, p->fused_first, p->fused_count, gathered, W, p->msg_bytes,

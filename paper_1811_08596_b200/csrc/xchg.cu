@@ -95,6 +95,7 @@ struct fgc_exchange {
   std::vector<cudaEvent_t> ev;        // per piece: compress done on the caller's stream
   cudaEvent_t ev_copies = nullptr;
   uint32_t counter = 0;               // pieces published so far
+  uint32_t pexp[kMaxPieces] = {};     // host copy of what pcnt[i] reaches once the queued compresses finish
   uint64_t step = 0;
   bool opened = false;
 };
@@ -315,6 +316,11 @@ PieceWait exchange_piece_wait(fgc_exchange* x, uint32_t first, uint32_t per, uin
 }
 
 uint32_t exchange_max_pieces() { return kMaxPieces; }
+
+// The counter value piece i reaches once a compress that adds `chunks`
+// finished chunks to it completes (steps that bypass the counters -- the
+// host-buffer step -- leave the targets alone).
+uint32_t exchange_piece_target(fgc_exchange* x, uint32_t i, uint32_t chunks) { return x->pexp[i] += chunks; }
 
 // Join the copy streams back into s (the caller's step is complete only when
 // its pushes are).
