@@ -40,7 +40,13 @@ def as_signal(values, name: str = "gradient"):
             a = np.asarray(values, dtype=np.float64)
         t = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     code = _lib.DTYPE_F32 if t.dtype == torch.float32 else _lib.DTYPE_F64
-    return t, code
+    return aligned(t), code
+
+
+def aligned(t: torch.Tensor) -> torch.Tensor:
+    """The kernels load two samples at a time: a view starting off an 8-byte
+    (f32) / 16-byte (f64) boundary is copied to a fresh allocation."""
+    return t.clone() if t.data_ptr() % (2 * t.element_size()) else t
 
 
 def flags_tensor() -> torch.Tensor:

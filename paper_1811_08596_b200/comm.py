@@ -188,6 +188,7 @@ class GradientAverager:
         code = _lib.DTYPE_F64 if grad.dtype == torch.float64 else _lib.DTYPE_F32
         if grad.dtype not in (torch.float32, torch.float64):
             raise ValueError("gradient must be float32 or float64")
+        grad = D.aligned(grad.contiguous())
         dst = self.out if out is None else out
         if self.exchange is not None:
             _lib.check(_lib.lib.fgc_exchange_average(self.plan.handle, self.exchange.handle, grad.data_ptr(), code,

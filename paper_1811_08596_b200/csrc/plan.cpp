@@ -29,6 +29,23 @@ using RealClass = RealClassT<float>;
 
 static uint64_t a16(uint64_t x) { return (x + 15) & ~15ull; }
 
+// The transform kernels load the signal two samples at a time (float2 /
+// double2), so a device gradient must be 8-byte (f32) or 16-byte (f64)
+// aligned.
+static fgc_status check_signal(const void* g, int dtype) {
+  if (dtype != FGC_DTYPE_F32 && dtype != FGC_DTYPE_F64) {
+    set_error("unknown dtype");
+    return FGC_ERR_INVALID;
+  }
+  const uintptr_t need = dtype == FGC_DTYPE_F64 ? 16 : 8;
+  if (reinterpret_cast<uintptr_t>(g) % need) {
+    set_error(dtype == FGC_DTYPE_F64 ? "float64 gradient must be 16-byte aligned"
+                                     : "float32 gradient must be 8-byte aligned");
+    return FGC_ERR_INVALID;
+  }
+  return FGC_OK;
+}
+
 }  // namespace fgc
 
 using namespace fgc;
@@ -368,6 +385,7 @@ extern "C" fgc_status fgc_compress(fgc_plan* p, const void* grad, int dtype, uin
                                    void* stream) {
   if (!p || !grad || !message || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
   FGC_TRY(check_mode(p));
+  FGC_TRY(check_signal(grad, dtype));
   if (p->desc.mode == FGC_MODE_ENERGY)
     return energy_compress(p, grad, dtype, nullptr, message, nullptr, flags, static_cast<cudaStream_t>(stream));
   return compress_range(p, grad, dtype, message, flags, static_cast<cudaStream_t>(stream), p->fused_first,
@@ -388,6 +406,7 @@ extern "C" fgc_status fgc_encode_spectrum(fgc_plan* p, const void* spectrum, uin
 extern "C" fgc_status fgc_forward_spectrum(fgc_plan* p, const void* grad, int dtype, void* spectrum, uint32_t* flags,
                                            void* stream) {
   if (!p || !grad || !spectrum || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_signal(grad, dtype));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (RealClass& rc : p->classes) {
     if (!rc.fused) continue;
@@ -618,6 +637,7 @@ extern "C" fgc_status fgc_allgather_average(fgc_plan* p, void* comm, int nranks,
   }
   if (!comm || !gathered) { set_error("multi-rank average needs a communicator and a gather buffer"); return FGC_ERR_INVALID; }
   FGC_TRY(check_mode(p));
+  FGC_TRY(check_signal(grad, dtype));
   Weights w;
   FGC_TRY(fill_weights(weights, nranks, w));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -697,6 +717,7 @@ extern "C" fgc_status fgc_exchange_average(fgc_plan* p, fgc_exchange* x, const v
   if (!p || !x || !grad || !out || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
   if (!exchange_ready(x)) { set_error("exchange not opened"); return FGC_ERR_INVALID; }
   FGC_TRY(check_mode(p));
+  FGC_TRY(check_signal(grad, dtype));
   uint32_t* counter;
   uint64_t* step;
   int W, me;
@@ -789,8 +810,8 @@ extern "C" fgc_status fgc_average_host(fgc_plan* p, fgc_exchange* x, const void*
     set_error("null argument");
     return FGC_ERR_INVALID;
   }
-  if (dtype != FGC_DTYPE_F32 && dtype != FGC_DTYPE_F64) { set_error("unknown dtype"); return FGC_ERR_INVALID; }
   FGC_TRY(check_mode(p));
+  FGC_TRY(check_signal(dev_grad, dtype));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int W = 1, me = 0;
   uint32_t* counter = nullptr;

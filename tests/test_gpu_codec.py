@@ -652,3 +652,24 @@ def test_step_host_matches_device_step(n, mode, dt):
     avg.check()
     want = O.decompress(O.from_wire(F.serialize(F.compress(g, avg.config))))
     assert rel_l2(ref.double().numpy(), want) <= 1e-5
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_unaligned_views_are_realigned(dt):
+    """A tensor view starting off the kernels' two-sample alignment is copied
+    by the Python layer; the C ABI rejects such a pointer instead of faulting."""
+    from paper_1811_08596_b200 import _lib
+    n = 65536 + 333
+    base = (torch.randn(n + 1, dtype=torch.float64, device="cuda") * 1e-2).to(dt)
+    view = base[1:]
+    cfg = F.CodecConfig(F.SparsificationSpec(0.9), F.calibrate([view.cpu().numpy()], 8, 3))
+    got = F.reconstruct(view, cfg)
+    ref = F.reconstruct(view.clone(), cfg)
+    np.testing.assert_array_equal(got, ref)
+    plan = F.codec.get_plan(n, cfg.chunk_size, 0.9, "count", False, cfg.quantizer)
+    msg = plan.new_message()
+    fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+    code = _lib.DTYPE_F64 if dt == torch.float64 else _lib.DTYPE_F32
+    st = _lib.lib.fgc_compress(plan.handle, view.data_ptr(), code,
+                               msg.data_ptr(), fl.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert st != 0 and "aligned" in _lib.lib.fgc_last_error().decode()
