@@ -70,6 +70,30 @@ def main():
                 "csv_sha256": hashlib.sha256(tr.to_csv_bytes()).hexdigest()}
         out["cases"].append(case)
         print(name, "final loss", tr.loss[-1], "max err_ratio", float(tr.err_ratio.max()))
+    # the `simulate` subcommand (cli.py:268-345, 407-435): summary line + CSV bytes
+    import contextlib
+    import io
+    import os
+    import tempfile
+    import importlib
+    ref_cli = importlib.import_module("fgc_ref.cli")
+    out["cli"] = []
+    for argv in (["simulate", "--theta0", "0", "--iters", "50", "--workers", "2"],
+                 ["simulate", "--problem", "logistic", "--nbits", "8", "--iters", "40", "--theta-schedule",
+                  "diminishing", "--lr-schedule", "diminishing", "--lr-tau", "10"],
+                 ["simulate", "--problem", "mlp", "--nbits", "6", "--mantissa", "2", "--iters", "30",
+                  "--theta0", "0.7", "--seed", "11"]):
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "trace.csv")
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                code = ref_cli.dispatch(argv + ["--out", path])
+            csv_bytes = open(path, "rb").read()
+        summary = json.loads(buf.getvalue().strip().splitlines()[-1])
+        summary.pop("out")
+        out["cli"].append({"argv": argv, "code": code, "summary": summary,
+                           "csv_sha256": hashlib.sha256(csv_bytes).hexdigest(),
+                           "loss": [float(r.split(b",")[1]) for r in csv_bytes.splitlines()[1:]]})
     (HERE / "sim_golden.json").write_text(json.dumps(out, indent=1) + "\n")
 
 

@@ -101,3 +101,48 @@ def test_inspect_and_quantizer_dump(capsys, tmp_path):
     lat = O.lattice(s["min"], s["max"], 8, 3, s["eps"])
     vals = np.array([float(x.split(",")[1]) for x in lines[1:]])
     np.testing.assert_array_equal(vals, O.dequantize(lat, np.arange(256)))
+
+
+# ---------------------------------------------------------------- simulate (cli.py:268-345)
+import hashlib  # noqa: E402
+from pathlib import Path  # noqa: E402
+
+SIM_CLI = json.loads((Path(__file__).resolve().parent / "golden" / "sim_golden.json").read_text())["cli"]
+
+
+def _simulate(capsys, tmp_path, rec):
+    out = tmp_path / "trace.csv"
+    code, s, _ = run(capsys, *rec["argv"], "--out", str(out))
+    s.pop("out")
+    return code, s, out.read_bytes()
+
+
+def test_simulate_bypass_matches_reference_bytes(capsys, tmp_path):
+    rec = SIM_CLI[0]                    # theta 0, passthrough: plain SGD, no codec
+    code, s, csv_bytes = _simulate(capsys, tmp_path, rec)
+    assert code == rec["code"] and s == rec["summary"]
+    assert hashlib.sha256(csv_bytes).hexdigest() == rec["csv_sha256"]
+
+
+def test_simulate_config_file_and_errors(capsys, tmp_path, monkeypatch):
+    cfg = tmp_path / "c.json"
+    cfg.write_text(json.dumps({"iters": 5, "theta0": 0.0, "bogus": 1}))
+    code, s, _ = run(capsys, "simulate", "--config", str(cfg))
+    assert code == 2 and s["status"] == "error" and "bogus" in s["error"]
+    cfg.write_text(json.dumps({"iters": 5, "theta0": 0.0}))
+    monkeypatch.setenv("FGC_SEED", "17")
+    code, s, _ = run(capsys, "simulate", "--config", str(cfg))
+    assert code == 0 and s["iterations"] == 5 and s["seed"] == 17
+    code, _, _ = run(capsys, "simulate", "--channel", "pigeon")
+    assert code == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("i", [1, 2])
+def test_simulate_compressed_follows_reference(capsys, tmp_path, i):
+    rec = SIM_CLI[i]
+    code, s, csv_bytes = _simulate(capsys, tmp_path, rec)
+    assert code == rec["code"] and s["iterations"] == rec["summary"]["iterations"]
+    loss = [float(r.split(b",")[1]) for r in csv_bytes.splitlines()[1:]]
+    np.testing.assert_allclose(loss, rec["loss"], rtol=1e-6, atol=0)
+    assert s["final_loss"] == pytest.approx(rec["summary"]["final_loss"], rel=1e-6)
