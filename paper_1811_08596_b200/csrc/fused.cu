@@ -76,8 +76,13 @@ constexpr uint32_t kBins = kN + 1;                     // 32769
 constexpr uint32_t kBmWords = (2 * kBins + 31) / 32;  // 2049
 constexpr uint32_t kHalfBins = kN / 2;                 // 16384: pack split point
 constexpr uint32_t kStageOff = 16900;                  // u32 offset of the code-stream staging in buf
+// emit-phase compaction strips (per warp: 256 bins + 256 float2) above the code half
+constexpr uint32_t kEmitStageOff = 16904;
+constexpr uint32_t kEmitStageWords = 768;
 static_assert(kStageOff > (kHalfBins + kHalfBins / 32) &&
               kStageOff + (32 + (kHalfBins + 1) * 32 + 31) / 32 <= 2 * (kPadded + 64), "staging fits in buf");
+static_assert(kEmitStageOff % 2 == 0 && kEmitStageOff >= kHalfBins + kHalfBins / 32 &&
+              kEmitStageOff + 16 * kEmitStageWords <= 2 * (kPadded + 64), "emit strips fit in buf");
 
 template <int B, int E, class F>
 __device__ __forceinline__ void static_for(F&& f) {
@@ -563,11 +568,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       }
     }
   };
+  // keep bits first, branch-free across all 32 values (bit 2j: va[j], 2j+1: vb[j])
+  uint32_t keep = 0, band = 0;
   static_for<0, 16>([&](auto J) {
     constexpr int j = decltype(J)::value;
-    emit_pair(va[j], BIN_A(j), std::integral_constant<uint32_t, (j >= 8 ? 1u : 0u)>{});
-    emit_pair(vb[j], BIN_B(j), std::integral_constant<uint32_t, (j >= 8 ? 1u : 0u)>{});
+    const float pa = proxy_key(va[j].x, va[j].y), pb = proxy_key(vb[j].x, vb[j].y);
+    keep |= ((pa >= hi_b ? 1u : 0u) << (2 * j)) | ((pb >= hi_b ? 1u : 0u) << (2 * j + 1));
+    band |= ((pa >= lo_b && pa < hi_b ? 1u : 0u) << (2 * j)) | ((pb >= lo_b && pb < hi_b ? 1u : 0u) << (2 * j + 1));
   });
+  while (band) {                                  // undecided bins: the resolved list decides
+    const uint32_t b = __ffs(band) - 1u;
+    band &= band - 1u;
+    const uint32_t bin = 2u * (((b & 1u) ? kb : ka) + 1024u * (b >> 1)) + r;
+    if (!inband_dropped(&sh0, mcount, bin)) keep |= 1u << b;
+  }
+  // Only ~1 value in 10 is kept, so encoding every value in every lane would
+  // spend most of the phase on dropped bins.  Per round of 4 j (8 values per
+  // lane) the warp compacts its kept (bin, value) pairs into a staging strip
+  // of the free upper part of buf, then every lane encodes and stores
+  // consecutive entries.  Rounds 0-1 land in half 0, rounds 2-3 in half 1.
+  {
+    const uint32_t lane = tid & 31u;
+    uint32_t* wmeta = arr_own + kEmitStageOff + (tid >> 5) * kEmitStageWords;
+    float2* wval = reinterpret_cast<float2*>(wmeta + 256);
+    static_for<0, 4>([&](auto R) {
+      constexpr int j0 = 4 * decltype(R)::value;
+      constexpr uint32_t d = j0 >= 8 ? 1u : 0u;
+      const uint32_t m8 = (keep >> (2 * j0)) & 0xFFu;
+      const uint32_t cnt = __popc(m8);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      uint32_t pos = incl - cnt;
+      static_for<0, 8>([&](auto K) {
+        constexpr int k = decltype(K)::value;
+        constexpr int j = j0 + k / 2;
+        if ((m8 >> k) & 1u) {
+          wmeta[pos] = (k & 1) ? BIN_B(j) : BIN_A(j);
+          wval[pos] = (k & 1) ? vb[j] : va[j];
+          ++pos;
+        }
+      });
+      __syncwarp();
+      for (uint32_t e = lane; e < total; e += 32) {
+        const uint32_t bin = wmeta[e];
+        const float2 x = wval[e];
+        const uint32_t cre = enc16(q, x.x), cim = enc16(q, x.y);
+        const uint32_t pc = cre | (cim << 16);
+        if (pc) {
+          const uint32_t c = (cre ? 1u : 0u) + (cim ? 1u : 0u);
+          if (d) rc1 += c; else rc0 += c;
+          const uint32_t lb = bin - d * kHalfBins;
+          const uint32_t bits = ((cre ? 1u : 0u) | (cim ? 2u : 0u)) << (2u * (lb & 15u));
+          if (d == r) {
+            arr_own[pad(lb)] = pc;
+            atomicOr(&sh.hbm[lb >> 4], bits);
+          } else {
+            arr_peer[pad(lb)] = pc;
+            atomicOr(&shp.hbm[lb >> 4], bits);
+          }
+        }
+      }
+      __syncwarp();                               // strip reused by the next round
+    });
+  }
   if (special) emit_pair(xn, kN, std::integral_constant<uint32_t, 1u>{});
 #undef BIN_A
 #undef BIN_B
