@@ -26,12 +26,17 @@ constexpr int kSelThreads = 512;
 constexpr int kCandCap = 1024;
 constexpr uint32_t kHistBins = 2048;
 
+constexpr int kPer = 4;                                   // bins per thread per final-pass tile
+constexpr uint32_t kTile = kPer * kSelThreads;
+constexpr uint32_t kStageWords = 2 * kTile + 4;           // one tile of codes (<= 2 kTile codes * 32 bits)
+static_assert(16 % kPer == 0 || kPer == 16, "a lane group owns whole bitmap words");
+
 struct SelectShared {
   uint32_t hist[kHistBins];
   uint32_t scan[40];
   unsigned long long key[kCandCap];
   uint32_t idx[kCandCap];
-  uint32_t stage[2 * kSelThreads * 32 / 32 + 4];   // one tile of codes (<= 2T codes * 32 bits)
+  uint32_t stage[kStageWords];
   uint32_t cnt;
   uint32_t found_bucket, found_below;
 };
@@ -55,20 +60,21 @@ struct Coeffs<double2> {
   }
 };
 
-// Visit every bin of the chunk, each thread 4 bins per round with their loads
-// issued together (the passes are latency-bound on these loads otherwise).
+// Visit every bin of the chunk, each thread kFly bins per round with their
+// loads issued together (the passes are latency-bound on these loads otherwise).
+constexpr int kFly = 4;
 template <typename CT, typename F>
 __device__ __forceinline__ void for_bins(const Coeffs<CT>& cf, uint32_t B, F&& f) {
-  for (uint32_t i0 = threadIdx.x; i0 < B; i0 += 4 * kSelThreads) {
-    float re[4], im[4];
-    double dr[4], di[4];
+  for (uint32_t i0 = threadIdx.x; i0 < B; i0 += kFly * kSelThreads) {
+    float re[kFly], im[kFly];
+    double dr[kFly], di[kFly];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kFly; ++u) {
       const uint32_t i = i0 + u * kSelThreads;
       if (i < B) cf.get(i, re[u], im[u], dr[u], di[u]);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kFly; ++u) {
       const uint32_t i = i0 + u * kSelThreads;
       if (i < B) f(i, re[u], im[u], dr[u], di[u]);
     }
@@ -257,7 +263,10 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
     }
   }
 
-  // ---- final pass: decide, quantize, bitmap + code stream (tile-sequential)
+  // ---- final pass: decide, quantize, bitmap + code stream.  Tiles of
+  //      kPer * kSelThreads bins, each thread kPer consecutive bins (so its
+  //      codes are consecutive in the stream and a lane pair owns one bitmap
+  //      word); one block scan per tile places every thread's codes.
   uint32_t* seg = reinterpret_cast<uint32_t*>(message + ci.seg_off);
   uint32_t* bitmap = seg + kSegHeader / 4;
   uint32_t* codes = reinterpret_cast<uint32_t*>(message + ci.seg_off + ci.code_off);
@@ -267,92 +276,96 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
   uint32_t origin = 0;        // global code word index of stage[0]
   uint32_t tie_seen = 0;
   bool overflow = false;
-  const uint32_t stage_words = 2 * kSelThreads * 32 / 32 + 4;
-  for (uint32_t s = tid; s < stage_words; s += kSelThreads) sh.stage[s] = 0;
+  for (uint32_t s = tid; s < kStageWords; s += kSelThreads) sh.stage[s] = 0;
   __syncthreads();
 
-  float nre = 0.f, nim = 0.f; double ndr = 0.0, ndi = 0.0;   // the next tile's bin, loaded a tile ahead
-  if (tid < B) cf.get(tid, nre, nim, ndr, ndi);
-  for (uint32_t t0 = 0; t0 < B; t0 += kSelThreads) {
-    const uint32_t i = t0 + tid;
-    const bool valid = i < B;
-    const float re = nre, im = nim;
-    const double dr = ndr, di = ndi;
-    if (i + kSelThreads < B) cf.get(i + kSelThreads, nre, nim, ndr, ndi);
-    bool dropped = false;
-    bool is_tie = false;
-    unsigned long long key = 0;
-    if (mode == kDropAll) {
-      dropped = true;
-    } else if (mode == kMask) {
-      dropped = valid && drop_mask[ci.bin_off + i];
-    } else if (mode == kList || mode == kExact) {
-      const float p = proxy_key(re, im);
-      const bool inband = all_band || (p >= band_lo && p < band_hi);
-      if (!all_band && p < band_lo) dropped = true;
-      else if (inband && valid) {
-        if (mode == kList) {
-          uint32_t lo = 0, hi = m;                 // binary search by index
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if ((sh.idx[mid] & 0x7FFFFFFFu) < i) lo = mid + 1; else hi = mid;
+  for (uint32_t t0 = 0; t0 < B; t0 += kTile) {
+    const uint32_t i0 = t0 + tid * kPer;
+    float re[kPer], im[kPer];
+    double dr[kPer], di[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      re[u] = im[u] = 0.f;
+      dr[u] = di[u] = 0.0;
+      if (i0 + u < B) cf.get(i0 + u, re[u], im[u], dr[u], di[u]);
+    }
+    bool dropped[kPer], is_tie[kPer];
+    uint32_t ntie = 0;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t i = i0 + u;
+      const bool valid = i < B;
+      dropped[u] = false;
+      is_tie[u] = false;
+      if (mode == kDropAll) {
+        dropped[u] = true;
+      } else if (mode == kMask) {
+        dropped[u] = valid && drop_mask[ci.bin_off + i];
+      } else if (mode == kList || mode == kExact) {
+        const float p = proxy_key(re[u], im[u]);
+        const bool inband = all_band || (p >= band_lo && p < band_hi);
+        if (!all_band && p < band_lo) dropped[u] = true;
+        else if (inband && valid) {
+          if (mode == kList) {
+            uint32_t lo = 0, hi = m;                 // binary search by index
+            while (lo < hi) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if ((sh.idx[mid] & 0x7FFFFFFFu) < i) lo = mid + 1; else hi = mid;
+            }
+            dropped[u] = (lo < m) && ((sh.idx[lo] & 0x7FFFFFFFu) == i) && (sh.idx[lo] & 0x80000000u);
+          } else if (need > 0) {
+            const unsigned long long key = (unsigned long long)__double_as_longlong(cabs_key(dr[u], di[u]));
+            dropped[u] = key < Te;
+            is_tie[u] = key == Te;
+            ntie += is_tie[u] ? 1u : 0u;
           }
-          dropped = (lo < m) && ((sh.idx[lo] & 0x7FFFFFFFu) == i) && (sh.idx[lo] & 0x80000000u);
-        } else if (need > 0) {
-          key = (unsigned long long)__double_as_longlong(cabs_key(dr, di));
-          dropped = key < Te;
-          is_tie = key == Te;
         }
       }
+      if (!valid) dropped[u] = true;
     }
-    if (mode == kExact) {
+    if (mode == kExact) {                        // ties dropped in bin order up to tie_cut
       uint32_t ties_total;
-      const uint32_t tie_rank = tie_seen + block_exclusive_scan<kSelThreads>(is_tie ? 1u : 0u, sh.scan, ties_total);
-      if (is_tie) dropped = tie_rank < tie_cut;
+      uint32_t tr = tie_seen + block_exclusive_scan<kSelThreads>(ntie, sh.scan, ties_total);
+#pragma unroll
+      for (int u = 0; u < kPer; ++u)
+        if (is_tie[u]) dropped[u] = tr++ < tie_cut;
       tie_seen += ties_total;
     }
-    if (!valid) dropped = true;
-    const uint32_t cre = dropped ? 0u : encode_code(q, re);
-    const uint32_t cim = dropped ? 0u : encode_code(q, im);
-    if (kept_mask && valid) kept_mask[ci.bin_off + i] = dropped ? 0 : 1;
-
-    const uint32_t bre = __ballot_sync(0xffffffffu, cre != 0u);
-    const uint32_t bim = __ballot_sync(0xffffffffu, cim != 0u);
-    // bitmap words for the warp's 64 slots
-    if (lane < 2) {
-      const uint32_t rh = lane ? (bre >> 16) : (bre & 0xFFFFu);
-      const uint32_t ih = lane ? (bim >> 16) : (bim & 0xFFFFu);
-      const uint32_t w = spread16(rh) | (spread16(ih) << 1);
-      const uint32_t widx = (t0 + warp * 32) / 16 + lane;
-      if (widx < bm_words) bitmap[widx] = ballot_to_wire(w);
+    uint32_t cre[kPer], cim[kPer];
+    uint32_t cnt = 0, nat = 0;                   // my codes; my 2*kPer slot bits in natural order
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      cre[u] = dropped[u] ? 0u : encode_code(q, re[u]);
+      cim[u] = dropped[u] ? 0u : encode_code(q, im[u]);
+      if (kept_mask && i0 + u < B) kept_mask[ci.bin_off + i0 + u] = dropped[u] ? 0 : 1;
+      cnt += (cre[u] ? 1u : 0u) + (cim[u] ? 1u : 0u);
+      nat |= ((cre[u] ? 1u : 0u) | (cim[u] ? 2u : 0u)) << (2 * u);
     }
-    // ranks
-    const uint32_t lt = lanemask_lt();
-    const uint32_t pre = __popc(bre & lt) + __popc(bim & lt);
-    const uint32_t wtot = __popc(bre) + __popc(bim);
-    if (lane == 0) sh.scan[warp] = wtot;
-    __syncthreads();
-    uint32_t wbase = 0, ttot = 0;
-    for (int w = 0; w < kSelThreads / 32; ++w) {
-      const uint32_t v = sh.scan[w];
-      if (w < warp) wbase += v;
-      ttot += v;
+    // bitmap: 32 slots per word = 32 / (2 kPer) threads per word
+    {
+      uint32_t w = nat;
+#pragma unroll
+      for (int o = 1; o < 16 / kPer; o <<= 1) w |= __shfl_down_sync(0xffffffffu, w, o) << (2 * kPer * o);
+      if ((lane & (16 / kPer - 1)) == 0) {
+        const uint32_t widx = i0 / 16;
+        if (widx < bm_words) bitmap[widx] = ballot_to_wire(w);
+      }
     }
-    const uint32_t r0 = rank_base + wbase + pre;
+    uint32_t ttot;
+    const uint32_t r0 = rank_base + block_exclusive_scan<kSelThreads>(cnt, sh.scan, ttot);
     // stage the codes (LSB-first N-bit fields, bit 0 of stage[0] = word `origin`)
     const uint64_t obit = (uint64_t)origin * 32u;
-    FGC_CHECK((uint64_t)(r0 + 2) * N - obit < 32ull * stage_words);
-    if (cre) {
-      const uint64_t lb = (uint64_t)r0 * N - obit;
-      const uint32_t o = (uint32_t)(lb & 31u);
-      atomicOr(&sh.stage[lb >> 5], cre << o);
-      if (o + N > 32u) atomicOr(&sh.stage[(lb >> 5) + 1], cre >> (32u - o));
-    }
-    if (cim) {
-      const uint64_t lb = (uint64_t)(r0 + (cre ? 1u : 0u)) * N - obit;
-      const uint32_t o = (uint32_t)(lb & 31u);
-      atomicOr(&sh.stage[lb >> 5], cim << o);
-      if (o + N > 32u) atomicOr(&sh.stage[(lb >> 5) + 1], cim >> (32u - o));
+    FGC_CHECK((uint64_t)(r0 + cnt) * N - obit <= 32ull * kStageWords);
+    uint64_t lb = (uint64_t)r0 * N - obit;
+#pragma unroll
+    for (int u = 0; u < 2 * kPer; ++u) {
+      const uint32_t c = (u & 1) ? cim[u >> 1] : cre[u >> 1];
+      if (c) {
+        const uint32_t o = (uint32_t)(lb & 31u);
+        atomicOr(&sh.stage[lb >> 5], c << o);
+        if (o + N > 32u) atomicOr(&sh.stage[(lb >> 5) + 1], c >> (32u - o));
+        lb += N;
+      }
     }
     __syncthreads();
     const uint64_t end_bit = (uint64_t)(rank_base + ttot) * N;
@@ -363,9 +376,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
     }
     const uint32_t carry = (full_end >= origin) ? sh.stage[full_end - origin] : 0u;
     __syncthreads();
-    for (uint32_t s = tid; s < stage_words; s += kSelThreads) sh.stage[s] = 0;
-    __syncthreads();
-    if (tid == 0) sh.stage[0] = carry;
+    for (uint32_t s = tid; s < kStageWords; s += kSelThreads) sh.stage[s] = (s == 0) ? carry : 0u;
     origin = full_end;
     rank_base += ttot;
     __syncthreads();
