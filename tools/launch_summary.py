@@ -15,7 +15,7 @@ agg = collections.OrderedDict()
 for d in data:
     if d["Metric Name"] != "gpu__time_duration.sum":
         continue
-    k = d["Kernel Name"].split("(")[0][:90]
+    k = d["Kernel Name"].split("(")[0][:80] + ("  grid " + d["Grid Size"] if d.get("Grid Size") else "")
     agg.setdefault(k, []).append(float(d["Metric Value"]))
 tot = sum(sum(v) for v in agg.values())
 print(f"{'launches':>8} {'mean_us':>10} {'total_us':>10} {'share':>6}  kernel")
