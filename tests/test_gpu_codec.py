@@ -463,31 +463,45 @@ def test_calibrate_matches_reference(golden):
 
 def test_resnet50_size_properties():
     """25.6M floats (BASELINE config 2): size-independent properties."""
-    n = 25_600_000
+    _size_properties(25_600_000, 0.9, (8, 3))
+
+
+@pytest.mark.parametrize("n,theta,nm", [
+    # BASELINE config 3: AlexNet-sized gradient, keep ratio 0.01 / 0.05 / 0.1 / 0.3
+    (61_000_000, 0.99, (8, 3)), (61_000_000, 0.95, (8, 3)), (61_000_000, 0.9, (8, 3)), (61_000_000, 0.7, (8, 3)),
+    # BASELINE config 4: VGG-16-sized gradient, 4/6/8/16-bit range floats
+    (138_000_000, 0.9, (4, 2)), (138_000_000, 0.9, (6, 2)), (138_000_000, 0.9, (8, 3)), (138_000_000, 0.9, (16, 9)),
+])
+def test_large_config_properties(n, theta, nm):
+    _size_properties(n, theta, nm)
+
+
+def _size_properties(n, theta, nm):
     g = torch.randn(n, device="cuda", generator=torch.Generator("cuda").manual_seed(0)) * 1e-2
-    q = F.calibrate([g[:65536 * 4].double().cpu().numpy()], 8, 3)
-    cfg = F.CodecConfig(F.SparsificationSpec(0.9), q)
+    q = F.calibrate([g[:65536 * 4].double().cpu().numpy()], *nm)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta), q)
     m1 = F.compress(g, cfg)
     m2 = F.compress(g, cfg)
     b1, b2 = debug.message_bytes(m1), debug.message_bytes(m2)
     assert b1 == b2                                   # deterministic
-    segs = segments_valid_bytes(b1, n, 65536, 0.9, 8)
+    segs = segments_valid_bytes(b1, n, 65536, theta, nm[0])
     for L, (nnz, bm, _) in zip(O.chunk_lengths(n, 65536), segs):
         bins = L // 2 + 1
-        assert nnz <= 2 * O.keep_bins(bins, 0.9)
-        assert bin(int.from_bytes(bm, "big")).count("1") == nnz
+        assert nnz <= 2 * O.keep_bins(bins, theta)
+        assert int.from_bytes(bm, "big").bit_count() == nnz
     out1 = F.codec.decompress_device(m1)
     out2 = F.codec.decompress_device(m2)
     assert torch.equal(out1, out2)
     # spot-check three chunks against the oracle decode of the same payloads
     host = g.double().cpu().numpy()
     spec = debug.forward_spectrum(g, cfg)
-    for c in (0, 200, 390):
+    last = len(O.chunk_lengths(n, 65536)) - 1
+    for c in (0, last // 2, last):
         L = O.chunk_lengths(n, 65536)[c]
         off = c * 65536
         b0 = c * 32769
-        _, ch = O.encode_spectrum(spec[b0:b0 + L // 2 + 1], L, 0.9, "count", lat_of(q))
-        ref = O.decompress(O.Message(L, 65536, 0.9, "count", False, lat_of(q), [ch]))
+        _, ch = O.encode_spectrum(spec[b0:b0 + L // 2 + 1], L, theta, "count", lat_of(q))
+        ref = O.decompress(O.Message(L, 65536, theta, "count", False, lat_of(q), [ch]))
         assert rel_l2(out1[off:off + L].cpu().numpy(), ref) <= 1e-5
         assert rel_l2(np.fft.rfft(host[off:off + L]), spec[b0:b0 + L // 2 + 1]) <= 1e-6
 
