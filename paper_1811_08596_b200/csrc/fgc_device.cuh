@@ -98,6 +98,11 @@ __device__ __forceinline__ uint32_t read_bits(const uint32_t* words, uint64_t po
   return width == 32 ? v : (v & ((1u << width) - 1u));
 }
 
+// Release store of a completion tag (pairs with an ld.acquire.gpu spin).
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -143,6 +143,8 @@ fgc_status real_inverse(RealClassT<R>& rc, const ChunkInfo* d_chunks, const type
 struct PieceCounter {
   uint32_t* cnt = nullptr;
   uint32_t first = 0, per = 1;
+  uint32_t* done = nullptr;           // per chunk id: set to `tag` (release) once the segment is written
+  uint32_t tag = 0;
 };
 
 // Decode-side wait of the peer exchange: before reading chunk c, every peer
@@ -151,6 +153,10 @@ struct PieceWait {
   const uint32_t* flags = nullptr;
   uint32_t stride = 0, first = 0, per = 1, target = 0;
   int nranks = 0, me = 0;
+  // this rank's own segment: done[c] == tag (the compress kernel of the same
+  // step runs concurrently; the decode is launched as its programmatic dependent)
+  const uint32_t* done = nullptr;
+  uint32_t tag = 0;
 };
 
 // drop_mask (may be null): 1 byte per bin of the chunk-major spectrum; when

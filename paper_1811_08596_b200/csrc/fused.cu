@@ -41,6 +41,7 @@
 #include "fgc_device.cuh"
 #include "fgc_internal.h"
 #include "fused_fft.cuh"
+#include "select_pack.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -292,6 +293,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   CompressShared& shp = *cluster.map_shared_rank(&sh, r ^ 1);
   const QuantParams q = a.q;
   const uint32_t dbg = g_fused_dbg;
+  // every CTA of the grid is resident or done from here on: the dependent
+  // decode grid may start filling SMs as they free up (it waits per chunk)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const T* g = static_cast<const T*>(a.grad) + ci.in_off;
 
   if (tid == 0) {
@@ -529,11 +533,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       out[BIN_B(j)] = vb[j];
     }
     if (special) out[kN] = xn;
-    if (r == 0 && tid == 0) a.fb[chunk] = 1u;
-    cluster.sync();          // peer finished reading sh0.mode before anyone exits
+    __threadfence();
+    cluster.sync();          // both halves written; the peer finished reading sh0.mode
+    if (r == 1) return;
+    // CTA 0 selects and packs the chunk with the generic single-CTA code,
+    // its scratch in the (now free) transpose buffer
+    static_assert(sizeof(sel::SelectShared) <= sizeof(sh.buf), "select scratch fits in buf");
+    sel::select_pack_chunk<float2>(*reinterpret_cast<sel::SelectShared*>(sh.buf), ci,
+                                   sel::Coeffs<float2>{a.fb_spec + ci.bin_off}, 0, q, a.message, nullptr, a.flags,
+                                   nullptr);
+    if (a.pc.cnt || a.pc.done) {
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        if (a.pc.cnt) atomicAdd(&a.pc.cnt[(chunk - a.pc.first) / a.pc.per], 1u);
+        if (a.pc.done) st_release_gpu(a.pc.done + chunk, a.pc.tag);
+      }
+    }
     return;
   }
-  if (r == 0 && tid == 0) a.fb[chunk] = 0u;
 
   // ---- 5. codes -> two bin-ordered halves: CTA 0 holds bins [0, 16384),
   //         CTA 1 holds [16384, 32768]; non-zero pairs only (arrays are zeroed).
@@ -742,12 +760,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     seg[1] = 0; seg[2] = 0; seg[3] = 0;
     if (used > ci.code_cap) atomicOr(a.flags, FGC_FLAG_CAPACITY);
   }
-  if (a.pc.cnt) {
+  if (a.pc.cnt || a.pc.done) {
     // the segment is complete once both CTAs' writes are visible device-wide
     __threadfence();
     if (!fold) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // the early arrive's phase
     cluster.sync();                               // (G) every thread of both CTAs has fenced
-    if (r == 0 && tid == 0) atomicAdd(&a.pc.cnt[(chunk - a.pc.first) / a.pc.per], 1u);
+    if (r == 0 && tid == 0) {
+      if (a.pc.cnt) atomicAdd(&a.pc.cnt[(chunk - a.pc.first) / a.pc.per], 1u);
+      if (a.pc.done) st_release_gpu(a.pc.done + chunk, a.pc.tag);
+    }
   } else if (fold) {
     cluster.sync();                               // G: CTA 0 finished reading CTA 1's staging
   } else {
@@ -854,6 +875,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   const uint32_t blk = dec_block(r, tid);                  // my 32-bin block
   const bool binN = (r == 0 && tid == kThreads - 1);       // also owns bin N (local slot 16384)
   float2* mine = acc + pad(32u * tid);                     // pad(32 t + j) = pad(32 t) + j
+  if (a.pw.done) {
+    // launched as the compress grid's programmatic dependent: wait until this
+    // rank's own segment of the chunk is written
+    if (tid == 0) {
+      const uint32_t* f = a.pw.done + chunk;
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v == a.pw.tag) break;
+        __nanosleep(256);
+      }
+    }
+    __syncthreads();
+  }
   if (a.pw.flags) {
     // peer exchange: every peer's copy of this chunk's piece has landed
     if (tid < (uint32_t)a.pw.nranks && (int)tid != a.pw.me) {
@@ -1186,7 +1221,23 @@ fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, 
   if (!count) return FGC_OK;
   DecodeArgs a{d_chunks, first, messages, W, stride, wts, q, out, t->thi, t->tlo, t->t1024, nullptr, count, t->wave,
                pw};
-  k_fused_decode<<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
+  if (pw.done) {
+    // programmatic dependent of the compress grid just launched on s: it may
+    // start once every compress CTA is resident, and waits per chunk
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * count);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sizeof(DecodeShared);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FGC_CUDA(cudaLaunchKernelEx(&cfg, k_fused_decode, a));
+  } else {
+    k_fused_decode<<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
+  }
   FGC_LAUNCHED(1);
   return FGC_OK;
 }

@@ -63,6 +63,8 @@ struct fgc_plan {
   float2* d_spec = nullptr;
   uint64_t* d_scratch = nullptr;
   uint32_t* d_fb = nullptr;          // per-chunk fused-kernel fallback flags
+  uint32_t* d_done = nullptr;        // per chunk: tag of the last compress that wrote its segment
+  uint32_t tag = 0;                  // last tag handed out
   cudaStream_t side = nullptr;       // generic (tail) classes overlap the fused kernels here
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   FusedTables* fused = nullptr;
@@ -92,6 +94,13 @@ static QuantParams make_qparams(const fgc_codec_desc& d) {
   q.pos_cap = d.quant.max;
   q.neg_cap = -d.quant.actual_min;
   return q;
+}
+
+// Decode overlapped with the compress grid's last wave (programmatic
+// dependent launch + per-chunk done tags); FGC_NO_OVERLAP=1 serialises them.
+static bool overlap_enabled() {
+  const char* e = getenv("FGC_NO_OVERLAP");
+  return !(e && e[0] == '1');
 }
 
 static bool fused_enabled() {
@@ -229,6 +238,10 @@ extern "C" fgc_status fgc_plan_create(const fgc_codec_desc* desc, fgc_plan** out
     return fail(cuda_check(e, "cudaMalloc"));
   if ((e = cudaMemset(p->d_fb, 0, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
     return fail(cuda_check(e, "cudaMemset"));
+  if ((e = cudaMalloc(&p->d_done, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
+    return fail(cuda_check(e, "cudaMalloc"));
+  if ((e = cudaMemset(p->d_done, 0, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
+    return fail(cuda_check(e, "cudaMemset"));
   {
     // the side stream carries the small tail-chunk kernels: give them priority
     // so they take SMs as soon as the wide fused kernels release any
@@ -266,6 +279,7 @@ extern "C" void fgc_plan_destroy(fgc_plan* p) {
   cudaFree(p->d_spec);
   cudaFree(p->d_scratch);
   cudaFree(p->d_fb);
+  cudaFree(p->d_done);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->side) cudaStreamDestroy(p->side);
@@ -369,10 +383,9 @@ static fgc_status compress_range(fgc_plan* p, const void* grad, int dtype, uint8
     }
   }
   if (fc) {
+    // (degenerate chunks are selected in place by the generic code, spectrum in d_spec)
     FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, f0, fc, grad, dtype, p->desc.half_pass, p->q, message,
                                   flags, p->d_fb, p->d_spec, s));
-    // degenerate chunks the fused select handed back (flag set, spectrum in d_spec)
-    FGC_TRY(launch_select_pack(p->d_chunks, f0, fc, p->d_spec, 0, p->q, message, nullptr, flags, s, p->d_fb));
   }
   if (fork) {
     FGC_CUDA(cudaEventRecord(p->ev_join, g));
@@ -632,8 +645,38 @@ extern "C" fgc_status fgc_allgather_average(fgc_plan* p, void* comm, int nranks,
                                             uint32_t* flags, void* stream) {
   if (!p || !grad || !message || !out || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
   if (nranks <= 1) {
-    FGC_TRY(fgc_compress(p, grad, dtype, message, flags, stream));
-    return fgc_decode_average(p, message, 1, p->msg_bytes, weights, out, stream);
+    if (!p->fused_count || p->desc.mode != FGC_MODE_COUNT || !overlap_enabled()) {
+      FGC_TRY(fgc_compress(p, grad, dtype, message, flags, stream));
+      return fgc_decode_average(p, message, 1, p->msg_bytes, weights, out, stream);
+    }
+    // one rank: generic chunks compress + decode on the side stream; the fused
+    // decode runs as the fused compress grid's programmatic dependent, each
+    // chunk's CTAs waiting for that chunk's segment (done tag)
+    FGC_TRY(check_mode(p));
+    FGC_TRY(check_signal(grad, dtype));
+    Weights w;
+    FGC_TRY(fill_weights(weights, 1, w));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool generic = p->classes.size() > 1;
+    if (generic) {
+      FGC_CUDA(cudaEventRecord(p->ev_fork, s));
+      FGC_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+      FGC_TRY(compress_range(p, grad, dtype, message, flags, p->side, 0, 0, true));
+      FGC_TRY(decode_range(p, message, 1, p->msg_bytes, w, out, p->side, 0, 0, true));
+      FGC_CUDA(cudaEventRecord(p->ev_join, p->side));
+    }
+    PieceCounter pc;
+    pc.done = p->d_done;
+    pc.tag = ++p->tag;
+    FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, p->fused_first, p->fused_count, grad, dtype,
+                                  p->desc.half_pass, p->q, message, flags, p->d_fb, p->d_spec, s, pc));
+    PieceWait pw;
+    pw.done = p->d_done;
+    pw.tag = pc.tag;
+    FGC_TRY(launch_fused_decode(p->fused, p->d_chunks, p->fused_first, p->fused_count, message, 1, p->msg_bytes, w,
+                                p->q, out, s, pw));
+    if (generic) FGC_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
+    return FGC_OK;
   }
   if (!comm || !gathered) { set_error("multi-rank average needs a communicator and a gather buffer"); return FGC_ERR_INVALID; }
   FGC_TRY(check_mode(p));
@@ -772,20 +815,29 @@ extern "C" fgc_status fgc_exchange_average(fgc_plan* p, fgc_exchange* x, const v
     P = std::min(std::min(P, Pmax), p->fused_count);
     const uint32_t per = (p->fused_count + P - 1) / P;
     P = (p->fused_count + per - 1) / per;
-    const PieceCounter pc = exchange_counter(x, p->fused_first, per);
+    PieceCounter pc = exchange_counter(x, p->fused_first, per);
+    const bool overlap = overlap_enabled();
+    if (overlap) {
+      pc.done = p->d_done;
+      pc.tag = ++p->tag;
+    }
     FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, p->fused_first, p->fused_count, grad, dtype,
                                   p->desc.half_pass, p->q, message, flags, p->d_fb, p->d_spec, s, pc));
-    FGC_TRY(launch_select_pack(p->d_chunks, p->fused_first, p->fused_count, p->d_spec, 0, p->q, message, nullptr,
-                               flags, s, p->d_fb, pc));
-    exchange_trace(s, "compressed");
     for (uint32_t i = 0; i < P; ++i) {
       const uint32_t c0 = p->fused_first + i * per, c1 = std::min(p->fused_first + p->fused_count, c0 + per);
       const uint64_t lo = p->seg_off[c0], hi = p->seg_off[c1];
       FGC_TRY(exchange_publish_piece(x, k, i, lo, hi - lo, exchange_piece_target(x, i, c1 - c0), tval));
     }
-    // one decode launch; each chunk's CTAs wait for their piece from every peer
+    // one decode launch, the compress grid's programmatic dependent: it fills
+    // the SMs the compress grid's last wave leaves idle; each chunk's CTAs wait
+    // for this rank's segment and for the piece from every peer
+    PieceWait pw = exchange_piece_wait(x, p->fused_first, per, tval);
+    if (overlap) {
+      pw.done = p->d_done;
+      pw.tag = pc.tag;
+    }
     FGC_TRY(launch_fused_decode(p->fused, p->d_chunks, p->fused_first, p->fused_count, gathered, W, p->msg_bytes,
-                                w, p->q, out, s, exchange_piece_wait(x, p->fused_first, per, tval)));
+                                w, p->q, out, s, pw));
     exchange_trace(s, "decoded");
   }
   if (generic) FGC_CUDA(cudaStreamWaitEvent(s, ev_side, 0));
