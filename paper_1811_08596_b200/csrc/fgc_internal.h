@@ -212,11 +212,11 @@ struct FusedTables;
 bool fused_available();
 fgc_status fused_tables_init(FusedTables** t, cudaStream_t s);
 void fused_tables_free(FusedTables* t);
-// fb: per-chunk fallback flags (1 = chunk left to the generic select kernel,
-// whose spectrum was written to fb_spec).
+// fb_spec: chunk-major spectrum scratch; a degenerate chunk's spectrum goes
+// there and CTA 0 selects it with the generic code in place.
 fgc_status launch_fused_compress(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                  const void* grad, int dtype, int half_pass, const QuantParams& q, uint8_t* message,
-                                 uint32_t* flags, uint32_t* fb, float2* fb_spec, cudaStream_t s,
+                                 uint32_t* flags, float2* fb_spec, cudaStream_t s,
                                  PieceCounter pc = PieceCounter());
 fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                const uint8_t* messages, int W, uint64_t stride, const Weights& wts,

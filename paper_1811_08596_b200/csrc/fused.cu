@@ -160,8 +160,7 @@ struct CompressArgs {
   const float2* thi;
   const float2* tlo;
   const float2* t1024;
-  uint32_t* fb;          // per-chunk fallback flag (indexed by chunk id)
-  float2* fb_spec;       // chunk-major spectrum scratch for fallback chunks
+  float2* fb_spec;       // chunk-major spectrum scratch for degenerate (fallback) chunks
   float2* dbg_spec;      // debug hook: write the spectrum and stop
   uint32_t count;        // chunks in this launch
   uint32_t ahead;        // L2 prefetch distance in chunks (one wave)
@@ -1173,10 +1172,10 @@ void fused_tables_free(FusedTables* t) {
 
 static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first,
                                        uint32_t count, const void* grad, int dtype, int half_pass,
-                                       const QuantParams& q, uint8_t* message, uint32_t* flags, uint32_t* fb,
+                                       const QuantParams& q, uint8_t* message, uint32_t* flags,
                                        float2* fb_spec, float2* dbg, cudaStream_t s, PieceCounter pc) {
   if (!count) return FGC_OK;
-  CompressArgs a{d_chunks, first, grad, q, message, flags, t->thi, t->tlo, t->t1024, fb, fb_spec, dbg, count, t->wave,
+  CompressArgs a{d_chunks, first, grad, q, message, flags, t->thi, t->tlo, t->t1024, fb_spec, dbg, count, t->wave,
                  pc};
   const size_t smem = sizeof(CompressShared);
   const dim3 grid(2 * count), block(kThreads);
@@ -1196,13 +1195,13 @@ static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_
 
 fgc_status launch_fused_compress(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                  const void* grad, int dtype, int half_pass, const QuantParams& q,
-                                 uint8_t* message, uint32_t* flags, uint32_t* fb, float2* fb_spec,
+                                 uint8_t* message, uint32_t* flags, float2* fb_spec,
                                  cudaStream_t s, PieceCounter pc) {
   if (q.n_bits > 16) {
     set_error("fused kernels take N <= 16");
     return FGC_ERR_UNSUPPORTED;
   }
-  return launch_compress_impl(t, d_chunks, first, count, grad, dtype, half_pass, q, message, flags, fb, fb_spec,
+  return launch_compress_impl(t, d_chunks, first, count, grad, dtype, half_pass, q, message, flags, fb_spec,
                               nullptr, s, pc);
 }
 
@@ -1211,7 +1210,7 @@ fgc_status launch_fused_spectrum(const FusedTables* t, const ChunkInfo* d_chunks
                                  cudaStream_t s) {
   QuantParams q{};
   q.n_bits = 8;
-  return launch_compress_impl(t, d_chunks, first, count, grad, dtype, half_pass, q, nullptr, flags, nullptr,
+  return launch_compress_impl(t, d_chunks, first, count, grad, dtype, half_pass, q, nullptr, flags,
                               nullptr, spectrum, s, PieceCounter());
 }
 

@@ -62,7 +62,6 @@ struct fgc_plan {
   ChunkInfo* d_chunks = nullptr;
   float2* d_spec = nullptr;
   uint64_t* d_scratch = nullptr;
-  uint32_t* d_fb = nullptr;          // per-chunk fused-kernel fallback flags
   uint32_t* d_done = nullptr;        // per chunk: tag of the last compress that wrote its segment
   uint32_t tag = 0;                  // last tag handed out
   cudaStream_t side = nullptr;       // generic (tail) classes overlap the fused kernels here
@@ -234,10 +233,6 @@ extern "C" fgc_status fgc_plan_create(const fgc_codec_desc* desc, fgc_plan** out
   if ((e = cudaMalloc(&p->d_spec, sizeof(float2) * p->spec_bins)) != cudaSuccess) return fail(cuda_check(e, "cudaMalloc"));
   if ((e = cudaMalloc(&p->d_scratch, sizeof(uint64_t) * (p->n_chunks + 1))) != cudaSuccess)
     return fail(cuda_check(e, "cudaMalloc"));
-  if ((e = cudaMalloc(&p->d_fb, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
-    return fail(cuda_check(e, "cudaMalloc"));
-  if ((e = cudaMemset(p->d_fb, 0, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
-    return fail(cuda_check(e, "cudaMemset"));
   if ((e = cudaMalloc(&p->d_done, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
     return fail(cuda_check(e, "cudaMalloc"));
   if ((e = cudaMemset(p->d_done, 0, sizeof(uint32_t) * p->n_chunks)) != cudaSuccess)
@@ -278,7 +273,6 @@ extern "C" void fgc_plan_destroy(fgc_plan* p) {
   cudaFree(p->d_chunks);
   cudaFree(p->d_spec);
   cudaFree(p->d_scratch);
-  cudaFree(p->d_fb);
   cudaFree(p->d_done);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
@@ -385,7 +379,7 @@ static fgc_status compress_range(fgc_plan* p, const void* grad, int dtype, uint8
   if (fc) {
     // (degenerate chunks are selected in place by the generic code, spectrum in d_spec)
     FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, f0, fc, grad, dtype, p->desc.half_pass, p->q, message,
-                                  flags, p->d_fb, p->d_spec, s));
+                                  flags, p->d_spec, s));
   }
   if (fork) {
     FGC_CUDA(cudaEventRecord(p->ev_join, g));
@@ -669,7 +663,7 @@ extern "C" fgc_status fgc_allgather_average(fgc_plan* p, void* comm, int nranks,
     pc.done = p->d_done;
     pc.tag = ++p->tag;
     FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, p->fused_first, p->fused_count, grad, dtype,
-                                  p->desc.half_pass, p->q, message, flags, p->d_fb, p->d_spec, s, pc));
+                                  p->desc.half_pass, p->q, message, flags, p->d_spec, s, pc));
     PieceWait pw;
     pw.done = p->d_done;
     pw.tag = pc.tag;
@@ -822,7 +816,7 @@ extern "C" fgc_status fgc_exchange_average(fgc_plan* p, fgc_exchange* x, const v
       pc.tag = ++p->tag;
     }
     FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, p->fused_first, p->fused_count, grad, dtype,
-                                  p->desc.half_pass, p->q, message, flags, p->d_fb, p->d_spec, s, pc));
+                                  p->desc.half_pass, p->q, message, flags, p->d_spec, s, pc));
     for (uint32_t i = 0; i < P; ++i) {
       const uint32_t c0 = p->fused_first + i * per, c1 = std::min(p->fused_first + p->fused_count, c0 + per);
       const uint64_t lo = p->seg_off[c0], hi = p->seg_off[c1];
