@@ -290,6 +290,31 @@ def test_fused_degenerate_and_mixed_chunks(theta):
     assert F.serialize(msg) == O.to_wire(om)
 
 
+@pytest.mark.parametrize("theta", [0.0, 0.5, 0.9, 1.0])
+def test_overlapped_average_with_degenerate_chunks(theta):
+    """The averaging step launches the decode as the compress grid's
+    programmatic dependent; chunks selected in place by the generic code
+    (tiny values), all-zero and tie-heavy chunks, over 200 chunks (several
+    waves) plus a tail, give the same bits as compress then decompress."""
+    from paper_1811_08596_b200.comm import GradientAverager
+    rng = np.random.default_rng(5)
+    L = 65536
+    g = (rng.standard_normal(200 * L + 999) * 1e-2).astype(np.float32)
+    g[3 * L:4 * L] = 0.0
+    g[50 * L:51 * L] = (rng.standard_normal(L) * 1e-30).astype(np.float32)
+    g[120 * L:121 * L] = 0.0
+    g[120 * L:121 * L:4096] = 1.0
+    g[199 * L:200 * L] = (rng.standard_normal(L) * 1e-30).astype(np.float32)
+    q = F.calibrate([g], 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta), q)
+    ref = F.codec.decompress_device(F.compress(g, cfg))
+    avg = GradientAverager(g.size, cfg, [1.0])
+    t = torch.from_numpy(g).cuda()
+    for _ in range(3):                          # tags advance per step
+        assert torch.equal(avg.step(t), ref)
+    avg.check()
+
+
 @pytest.mark.parametrize("W", [1, 3, 8])
 def test_fused_decode_average_matches_oracle(W):
     rng = np.random.default_rng(12 + W)
