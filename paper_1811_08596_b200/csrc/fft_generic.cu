@@ -98,10 +98,12 @@ __device__ T2* smem_stockham(T2* x, T2* y, uint32_t S, uint32_t nt, const T2* tw
   return x;
 }
 
-// Batched transforms of size S <= kSmemFftMax stored contiguously.
-template <class T2>
-__global__ void __launch_bounds__(kFftThreads) k_smem_fft(T2* data, uint32_t S, uint32_t per_cta, uint64_t total,
-                                                          const T2* tw, uint32_t twP, int dir) {
+// Batched transforms of size S <= kSmemFftMax stored contiguously.  NT
+// threads: 1024 when the batch is too small to fill the GPU (a tail chunk's
+// sub-transforms), where every radix-2 stage is latency-bound per thread.
+template <class T2, int NT>
+__global__ void __launch_bounds__(NT) k_smem_fft(T2* data, uint32_t S, uint32_t per_cta, uint64_t total,
+                                                 const T2* tw, uint32_t twP, int dir) {
   extern __shared__ __align__(16) unsigned char smraw[];
   T2* sm = reinterpret_cast<T2*>(smraw);
   const uint64_t first = (uint64_t)blockIdx.x * per_cta;
@@ -286,7 +288,11 @@ fgc_status pow2_rec(typename V2<R>::T* data, uint64_t batch, uint32_t P, const t
     // are spread over the SMs (latency, not throughput, rules there)
     const uint32_t per = max(1u, min(cap / P, (uint32_t)((batch + 295) / 296)));
     const size_t smem = 2ull * per * P * sizeof(T2);
-    k_smem_fft<T2><<<ceil_div(batch, per), kFftThreads, smem, s>>>(data, P, per, batch, tw, twP, dir);
+    const uint32_t ctas = ceil_div(batch, per);
+    if (ctas < 148 && P * per >= 4096)
+      k_smem_fft<T2, 1024><<<ctas, 1024, smem, s>>>(data, P, per, batch, tw, twP, dir);
+    else
+      k_smem_fft<T2, kFftThreads><<<ctas, kFftThreads, smem, s>>>(data, P, per, batch, tw, twP, dir);
     FGC_LAUNCHED(1);
     return FGC_OK;
   }
@@ -320,7 +326,8 @@ fgc_status set_attrs() {
   static bool done = false;
   if (done) return FGC_OK;
   const int bytes = (int)(2 * smem_points(sizeof(R)) * sizeof(T2));
-  FGC_CUDA(cudaFuncSetAttribute(k_smem_fft<T2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  FGC_CUDA(cudaFuncSetAttribute(k_smem_fft<T2, kFftThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  FGC_CUDA(cudaFuncSetAttribute(k_smem_fft<T2, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   FGC_CUDA(cudaFuncSetAttribute(k_col_fft<T2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   done = true;
   return FGC_OK;
