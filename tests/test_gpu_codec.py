@@ -669,6 +669,42 @@ def test_random_configs_match_oracle(seed):
     assert np.abs(got - ref).max() <= 1e-5 * scale, (n, chunk, theta, nm, mode)
 
 
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("FGC_SWEEP", "16"))))
+def test_random_averaging_step_matches_codec(seed):
+    """The one-rank averaging step (fused decode overlapped with the fused
+    compress, tail chunks on the side stream) gives the bits of compress then
+    decompress, over random sizes, keep ratios, lattices, dtypes and chunk
+    contents that hit every selection mode (zero, tiny, tie-heavy)."""
+    from paper_1811_08596_b200.comm import GradientAverager
+    rng = np.random.default_rng(5000 + seed)
+    L = 65536
+    nch = int(rng.integers(1, 160))
+    n = nch * L + int(rng.integers(0, L)) * int(rng.integers(0, 2))
+    theta = float(rng.choice([0.0, 0.5, 0.9, 0.97, 1.0]))
+    nm = [(8, 3), (4, 2), (6, 2), (16, 9)][int(rng.integers(0, 4))]
+    dt = np.float64 if rng.random() < 0.3 else np.float32
+    g = rng.standard_normal(n) * 10.0 ** rng.uniform(-4, 1)
+    for _ in range(int(rng.integers(0, 4))):       # special chunks
+        c = int(rng.integers(0, nch))
+        kind = int(rng.integers(0, 3))
+        if kind == 0:
+            g[c * L:(c + 1) * L] = 0.0
+        elif kind == 1:
+            g[c * L:(c + 1) * L] *= 1e-32
+        else:
+            g[c * L:(c + 1) * L] = 0.0
+            g[c * L:(c + 1) * L:int(rng.choice([1024, 4096, 8192]))] = 1.0
+    g = g.astype(dt)
+    q = F.calibrate([g], *nm)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta), q)
+    ref = F.codec.decompress_device(F.compress(g, cfg))
+    avg = GradientAverager(n, cfg, [1.0])
+    t = torch.from_numpy(g).cuda()
+    for _ in range(2):
+        assert torch.equal(avg.step(t), ref), (n, theta, nm, dt)
+    avg.check()
+
+
 # ---------------------------------------------------------------- host-buffer step
 @pytest.mark.parametrize("n,mode,dt", [(8 * 65536, "count", torch.float32), (20 * 65536 + 12345, "count", torch.float32),
                                        (3 * 65536 + 7, "count", torch.float64), (40000, "count", torch.float32),
