@@ -23,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, transport, mode, out_q):
+def _worker(rank, world, port, n, transport, mode, out_q, theta=0.9, nm=(8, 3), special=()):
     import torch.distributed as dist
 
     import oracle as O
@@ -37,8 +37,10 @@ def _worker(rank, world, port, n, transport, mode, out_q):
     try:
         rng = np.random.default_rng(77)
         rows = (rng.standard_normal((world, n)) * 1e-2).astype(np.float32)
-        q = F.calibrate([rows[0]], 8, 3)
-        cfg = F.CodecConfig(F.SparsificationSpec(0.9, mode), q)
+        for c, scale in special:                # zero / tiny chunks on rank 0
+            rows[0, c * 65536:(c + 1) * 65536] *= scale
+        q = F.calibrate([rows[0]], *nm)
+        cfg = F.CodecConfig(F.SparsificationSpec(theta, mode), q)
         comm = NcclComm()
         w = F.shard_weights(5 * world + 1, world)
         avg = GradientAverager(n, cfg, w, comm, transport=transport)
@@ -60,7 +62,8 @@ def _worker(rank, world, port, n, transport, mode, out_q):
         # own compress are bit-identical on all ranks, so serialize locally)
         msgs = [F.compress(rows[k], cfg) for k in range(world)]
         ref = sum(w[k] * O.decompress(O.from_wire(F.serialize(msgs[k]))) for k in range(world))
-        rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+        # a coarse lattice can zero every code (eps above every coefficient): then got must be 0 too
+        rel = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30))
         # every rank must hold bit-identical results
         digest = float(np.frombuffer(got.tobytes(), dtype=np.uint64).astype(np.float64).sum())
         out_q.put((rank, rel, digest))
@@ -86,4 +89,30 @@ def test_compressed_average_two_ranks(n, transport, mode):
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     res = [q.get(timeout=10) for _ in range(world)]
     assert all(rel <= 1e-5 for _, rel, _ in res), res
+    assert len({d for _, _, d in res}) == 1, "ranks disagree bitwise"
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_configs_two_ranks(seed):
+    """Random sizes, keep ratios and lattices over the peer exchange, with
+    degenerate chunks on one rank."""
+    import torch.multiprocessing as mp
+    rng = np.random.default_rng(70 + seed)
+    n = int(rng.integers(1, 120)) * 65536 + int(rng.integers(0, 65536))
+    theta = float(rng.choice([0.5, 0.9, 0.97]))
+    nm = [(8, 3), (4, 2), (16, 9)][int(rng.integers(0, 3))]
+    special = ((0, 0.0), (int(rng.integers(0, n // 65536)), 1e-32))
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, "peer", "count", q, theta, nm, special))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    res = [q.get(timeout=10) for _ in range(world)]
+    assert all(rel <= 1e-5 for _, rel, _ in res), (res, n, theta, nm)
     assert len({d for _, _, d in res}) == 1, "ranks disagree bitwise"
