@@ -330,6 +330,13 @@ const char* fgc_last_error(void);   /* thread-local message of the last failure 
 int         fgc_version(void);      /* 0xMMmmpp                                  */
 /* Count of device kernels launched by this process (instrumentation). */
 uint64_t    fgc_kernel_launches(void);
+/* Instrumentation for the roofline: launch ONLY the fused compress kernel of
+ * the plan's 65536-sample chunks (no tail chunk, no exchange) on `stream`;
+ * *alg_bytes = that launch's algorithmic bytes (signal read + segments
+ * written).  Not a codec entry point: the tail chunks' segments are left
+ * untouched. */
+fgc_status  fgc_profile_fused_compress(fgc_plan* plan, const void* grad, int dtype, uint8_t* message,
+                                       uint32_t* flags, void* stream, uint64_t* alg_bytes);
 
 #ifdef __cplusplus
 }

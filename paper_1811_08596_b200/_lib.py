@@ -100,6 +100,7 @@ _SIGS = {
     "fgc_exchange_message": (I32, [P, I32, C.POINTER(P), C.POINTER(P)]),
     "fgc_exchange_average": (I32, [P, P, P, I32, P, P, P, P]),
     "fgc_average_host": (I32, [P, P, P, I32, P, P, P, P, P, P, P]),
+    "fgc_profile_fused_compress": (I32, [P, P, I32, P, P, P, P]),
     "fgc_last_error": (C.c_char_p, []),
     "fgc_version": (I32, []),
     "fgc_kernel_launches": (U64, []),

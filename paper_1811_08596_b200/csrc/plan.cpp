@@ -994,6 +994,20 @@ extern "C" fgc_status fgc_average_host(fgc_plan* p, fgc_exchange* x, const void*
   return FGC_OK;
 }
 
+extern "C" fgc_status fgc_profile_fused_compress(fgc_plan* p, const void* grad, int dtype, uint8_t* message,
+                                                 uint32_t* flags, void* stream, uint64_t* alg_bytes) {
+  if (!p || !grad || !message || !flags || !alg_bytes) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_mode(p));
+  FGC_TRY(check_signal(grad, dtype));
+  *alg_bytes = 0;
+  if (!p->fused_count || p->desc.mode != FGC_MODE_COUNT) return FGC_OK;
+  const uint32_t f0 = p->fused_first, f1 = f0 + p->fused_count;
+  const uint64_t esz = dtype == FGC_DTYPE_F64 ? 8 : 4;
+  *alg_bytes = esz * 65536ull * p->fused_count + (p->seg_off[f1] - p->seg_off[f0]);
+  return launch_fused_compress(p->fused, p->d_chunks, f0, p->fused_count, grad, dtype, p->desc.half_pass, p->q,
+                               message, flags, p->d_spec, static_cast<cudaStream_t>(stream));
+}
+
 extern "C" const char* fgc_last_error(void) { return g_last_error.c_str(); }
 extern "C" int fgc_version(void) { return 0x000100; }
 extern "C" uint64_t fgc_kernel_launches(void) { return g_launches.load(); }
