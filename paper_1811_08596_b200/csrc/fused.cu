@@ -21,16 +21,19 @@
 //   each CTA emits its half of the MSB-first bitmap and of the LSB-first
 //   packed code stream (packer.py, quantizer.pack_codes) straight into the
 //   device message segment.  Degenerate chunks (all proxies tiny, or > kCand
-//   undecided bins) are handed to the generic select kernel via a flag.
+//   undecided bins) are selected in place by CTA 0 with the generic
+//   single-CTA code (select_pack.cuh) from the spectrum written to scratch.
 //
 // decode (k_fused_decode, 2 CTAs per chunk, 512 threads)
-//   CTA r builds Y_r (16384 complex, shared memory) directly from the W
-//   messages: every non-zero slot of bin b adds its weighted value into the
-//   two entries its bin feeds (Z[b] and Z[N-b], folded mod M), processed in
-//   four bin quarters so no two threads ever touch the same entry (fixed
-//   worker order -> deterministic, identical on every rank).  One inverse
-//   16384-point FFT per CTA then yields the even (r=0) or odd (r=1) complex
-//   samples of the chunk: x[4p+2r], x[4p+2r+1].
+//   Bins are owned in groups {k, M-k, M+k, N-k}; each thread accumulates the
+//   weighted non-zero slots of its 32-bin block from the W messages in
+//   worker order (single writer per entry: deterministic, identical on every
+//   rank).  Each CTA turns its groups into both CTAs' Y values, keeps its own
+//   and stores the peer's through DSMEM; one inverse 16384-point FFT per CTA
+//   then yields the even (r=0) or odd (r=1) complex samples of the chunk:
+//   x[4p+2r], x[4p+2r+1].  In the averaging step the decode is launched as
+//   the compress grid's programmatic dependent and waits per chunk for the
+//   segment's done tag (and, under the peer exchange, the peers' flags).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
