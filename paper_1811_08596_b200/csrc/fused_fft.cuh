@@ -141,9 +141,19 @@ __device__ __forceinline__ void fft_pass12(float2 (&v)[32], float2* buf, const f
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = r2[528 * j];
   const uint32_t k = i & 31u;
+  // W_1024^{jk}: odd j from the table, even j as W^{(j-1)k} W^k -- half the
+  // strided (bank-conflicting) table loads for one extra product
+  const float2 wk = t1024[tpad(k)];
+  float2 wprev = wk;
 #pragma unroll
-  for (int j = 1; j < 32; ++j) {                   // W_1024^{jk}, jk < 1024
-    float2 w = t1024[tpad(j * k)];
+  for (int j = 1; j < 32; ++j) {
+    float2 w;
+    if (j & 1) {
+      w = j == 1 ? wk : t1024[tpad(j * k)];
+      wprev = w;
+    } else {
+      w = cmul(wprev, wk);
+    }
     if (INV) w.y = -w.y;
     v[j] = cmul(v[j], w);
   }
