@@ -173,8 +173,20 @@ __device__ __forceinline__ void fft_pass3(uint32_t k, const float2* buf, float2 
   const float2* r3 = buf + k + (k >> 5);                // pad(k + 1024 j) = k + k/32 + 1056 j
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = r3[1056 * j];
+  // W_16384^{jk}: odd j from the two-level table, even j as W^{(j-1)k} W^k
+  const float2 wk = twc(thi, tlo, 4u * k, INV);
+  float2 wprev = wk;
 #pragma unroll
-  for (int j = 1; j < 16; ++j) v[j] = cmul(v[j], twc(thi, tlo, 4u * j * k, INV));    // W_16384^{jk}
+  for (int j = 1; j < 16; ++j) {
+    float2 w;
+    if (j & 1) {
+      w = j == 1 ? wk : twc(thi, tlo, 4u * j * k, INV);
+      wprev = w;
+    } else {
+      w = cmul(wprev, wk);
+    }
+    v[j] = cmul(v[j], w);
+  }
   dft<16, INV>(v);
 #pragma unroll
   for (int m = 0; m < 16; ++m) out[m] = v[bitrev(m, 4)];
