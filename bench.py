@@ -145,6 +145,41 @@ def cpu_reference(wl: dict, seconds_budget: float, cores: int | None = None, sam
     return gbs, cores, f"{sample_chunks} chunks x {chunk} floats ({sample_chunks * chunk} floats), {dt:.2f}s"
 
 
+def host_info() -> dict:
+    """CPU model, numpy version and SIMD dispatch line (BASELINE.md section 4
+    step 2), plus the H1 self-check: numpy's complex128 abs on THIS host
+    equals the cabs formula the selection key follows."""
+    import platform
+    info = {"numpy": np.__version__, "python": platform.python_version()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        from numpy._core import _multiarray_umath as mu
+        feats = mu.__cpu_features__
+        info["simd"] = {"baseline": list(mu.__cpu_baseline__),
+                        "found": [k for k in mu.__cpu_dispatch__ if feats.get(k)],
+                        "not_found": [k for k in mu.__cpu_dispatch__ if not feats.get(k)]}
+    except Exception as e:                          # noqa: BLE001
+        info["simd"] = f"unavailable: {e}"
+    try:
+        import oracle as O
+        rng = np.random.default_rng(11)
+        re = rng.standard_normal(20000) * np.exp2(rng.integers(-40, 40, 20000))
+        im = re * np.exp2(rng.integers(-30, 30, 20000)) * rng.choice([-1, 1], 20000)
+        im[:100] = 0.0
+        got = np.abs(re + 1j * im)
+        want = np.array([O.magnitude_exact(a, b) for a, b in zip(re, im)])
+        info["h1_cabs_selfcheck"] = {"values": int(re.size), "mismatches": int(np.count_nonzero(got != want))}
+    except Exception as e:                          # noqa: BLE001
+        info["h1_cabs_selfcheck"] = f"error: {e}"
+    return info
+
+
 def run_reference(args, wl, rank, world):
     if rank != 0:
         return
@@ -160,7 +195,8 @@ def run_reference(args, wl, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic gaussian sigma=1e-2",
             "config": workload_config(args, wl, world),
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample,
+                             "host": host_info()},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -348,6 +384,13 @@ def run_ours(args, wl, rank, world, local_rank):
                       "note": "unpipelined stage breakdown (NCCL allgather); ms_per_step is the public averaging "
                               "call, whose exchange overlaps the codec kernels"},
         "allreduce_fp32_ms": allreduce_ms,
+        "sync_vs_allreduce": (ms / allreduce_ms) if allreduce_ms else None,
+        "nvlink": {"bytes_in_per_rank": (world - 1) * M, "bytes_out_per_rank": (world - 1) * M,
+                   "achieved_gbs_per_rank": (world - 1) * M / (ms * 1e-3) / 1e9,
+                   "peak_gbs": 900.0, "peak_kind": "nominal per direction per GPU",
+                   "frac": (world - 1) * M / (ms * 1e-3) / 1e9 / 900.0,
+                   "measured_peer_copy_gbs": 770.0,
+                   "note": "allgather receive (W-1)*M per rank over the step time"},
         "message_bytes": M, "compression_ratio": 4.0 * n / M,
         "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
@@ -362,7 +405,8 @@ def run_ours(args, wl, rank, world, local_rank):
     }
     if world == 1 and not args.no_cpu_baseline:
         gbs, cores, sample = cpu_reference(wl, seconds_budget=15.0)
-        line["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample}
+        line["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample,
+                                "host": host_info()}
     print(json.dumps(line), flush=True)
 
 
@@ -381,9 +425,22 @@ def main():
     wl = dict(WORKLOADS[args.workload])
     if args.n:
         wl["n"] = args.n
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` outside torchrun: launch the N ranks ourselves
+        # (one process per GPU) and pass rank 0's JSON line through
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} ranks",
+              file=sys.stderr, flush=True)
     if args.impl == "reference":
         run_reference(args, wl, rank, world)
         return

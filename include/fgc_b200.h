@@ -90,8 +90,10 @@ fgc_status fgc_tune_eps(double min, double max, int n_bits, int mantissa_bits, d
 typedef struct fgc_codec_desc {
   uint64_t n;              /* gradient length (original_len)                */
   uint32_t chunk_size;     /* >= 16                                         */
-  int32_t  mode;           /* FGC_MODE_COUNT (FGC_MODE_ENERGY: unsupported) */
-  double   theta;          /* DROP ratio in [0,1] (float64, spectral.py:131)*/
+  int32_t  mode;           /* FGC_MODE_COUNT or FGC_MODE_ENERGY             */
+  double   theta;          /* DROP ratio in [0,1] (float64, spectral.py:131);
+                              count mode: also the capacity theta -- the
+                              plan accepts any runtime theta >= it         */
   int32_t  half_pass;      /* half_precision_pass                           */
   int32_t  passthrough;    /* 1: quantizer None, codes are raw f32 bits     */
   int32_t  full_capacity;  /* 1: size segments for every slot (messages not
@@ -131,6 +133,16 @@ fgc_status fgc_plan_get_info(const fgc_plan* plan, fgc_plan_info* out);
 fgc_status fgc_plan_segment_offsets(const fgc_plan* plan, uint64_t* offsets_host);
 /* Host array of n_chunks+1 bin offsets into a chunk-major spectrum. */
 fgc_status fgc_plan_bin_offsets(const fgc_plan* plan, uint64_t* offsets_host);
+
+/* Runtime theta: the drop ratio of the next compress calls on `stream`
+ * (the reference rebuilds its SparsificationSpec whenever the schedule moves
+ * theta, simulator.py:333-341, 522-528; here the plan, its message layout
+ * and any peer exchange stay).  Count mode: theta must not be below the
+ * plan's capacity theta (desc.theta at creation) unless the plan was
+ * created with full_capacity; energy mode: any theta in [0, 1].  The new
+ * per-chunk drop counts min(ceil(theta*bins), bins) (spectral.py:131) are
+ * written to the device chunk table on `stream` when they change. */
+fgc_status fgc_plan_set_theta(fgc_plan* plan, double theta, void* stream);
 
 /* ---- compress side (codec.compress, codec.py:220-243) ------------------ */
 

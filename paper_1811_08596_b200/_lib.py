@@ -61,6 +61,7 @@ _SIGS = {
     "fgc_plan_get_info": (I32, [P, C.POINTER(PlanInfo)]),
     "fgc_plan_segment_offsets": (I32, [P, P]),
     "fgc_plan_bin_offsets": (I32, [P, P]),
+    "fgc_plan_set_theta": (I32, [P, F64, P]),
     "fgc_compress": (I32, [P, P, I32, P, P, P]),
     "fgc_encode_spectrum": (I32, [P, P, P, P, P, P]),
     "fgc_forward_spectrum": (I32, [P, P, I32, P, P, P]),

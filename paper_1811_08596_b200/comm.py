@@ -25,7 +25,7 @@ import torch
 
 from . import _device as D
 from . import _lib
-from .codec import CodecConfig, _desc, get_plan
+from .codec import CodecConfig, Plan, _desc
 
 __all__ = ["message_layout", "shard_weights", "NcclComm", "PeerExchange", "GradientAverager", "allgather_average"]
 
@@ -142,10 +142,19 @@ class GradientAverager:
 
     transport "peer" (default; FGC_TRANSPORT overrides): pieces of the
     message move by peer-to-peer copies as soon as they are compressed and
-    are decoded as they land (PeerExchange).  "nccl": one ncclAllGather."""
+    are decoded as they land (PeerExchange).  "nccl": one ncclAllGather.
+
+    theta is a per-step argument (``step(grad, theta=...)``): the reference
+    rebuilds its SparsificationSpec whenever the schedule moves theta
+    (simulator.py:333-341, 522-528), here the plan, the message layout and
+    the exchange stay.  Messages are sized for ``capacity_theta`` (default:
+    the config's theta), the smallest drop ratio a step may ask for.
+
+    Every averager owns its plan (device scratch, done tags, side stream): a
+    plan is not safe on two streams at once (include/fgc_b200.h)."""
 
     def __init__(self, n: int, config: CodecConfig, weights, comm: NcclComm | None = None,
-                 transport: str | None = None):
+                 transport: str | None = None, capacity_theta: float | None = None):
         dev = D.require_cuda()
         spec = config.sparsification
         self.n = int(n)
@@ -156,8 +165,14 @@ class GradientAverager:
         if w.size != self.world:
             raise ValueError(f"need one weight per rank ({self.world}), got {w.size}")
         self.weights = np.ascontiguousarray(w)
-        self.plan = get_plan(self.n, config.chunk_size, spec.theta, spec.mode, config.half_precision_pass,
-                             config.quantizer)
+        cap = spec.theta if capacity_theta is None else float(capacity_theta)
+        if not 0.0 <= cap <= spec.theta:
+            raise ValueError(f"capacity_theta must be in [0, {spec.theta}], got {cap}")
+        self.capacity_theta = cap
+        self.plan = Plan(_desc(self.n, config.chunk_size, cap, spec.mode, config.half_precision_pass,
+                               config.quantizer, False))
+        self.theta = cap
+        self.set_theta(spec.theta)
         self.message = self.plan.new_message()
         self.gathered = (torch.empty(self.world * self.plan.message_bytes, dtype=torch.uint8, device=dev)
                          if self.world > 1 else self.message)
@@ -181,15 +196,31 @@ class GradientAverager:
             self.exchange.close()
             self.exchange = None
 
-    def step(self, grad: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def set_theta(self, theta: float) -> None:
+        """Drop ratio of the next steps (count mode: >= capacity_theta)."""
+        theta = float(theta)
+        if theta != self.theta:
+            _lib.check(_lib.lib.fgc_plan_set_theta(self.plan.handle, theta, D.stream()))
+            self.theta = theta
+
+    def _check_out(self, out: torch.Tensor) -> torch.Tensor:
+        if (not isinstance(out, torch.Tensor) or not out.is_cuda or out.device != self.out.device
+                or out.dtype != torch.float32 or out.numel() != self.n or not out.is_contiguous()):
+            raise ValueError("out must be a contiguous float32 CUDA tensor of the planned length "
+                             "on the averager's device")
+        return out
+
+    def step(self, grad: torch.Tensor, out: torch.Tensor | None = None, theta: float | None = None) -> torch.Tensor:
         """Average this rank's device gradient with every other rank's."""
         if grad.numel() != self.n or not grad.is_cuda:
             raise ValueError("gradient must be a CUDA tensor of the planned length")
         code = _lib.DTYPE_F64 if grad.dtype == torch.float64 else _lib.DTYPE_F32
         if grad.dtype not in (torch.float32, torch.float64):
             raise ValueError("gradient must be float32 or float64")
+        if theta is not None:
+            self.set_theta(theta)
         grad = D.aligned(grad.contiguous())
-        dst = self.out if out is None else out
+        dst = self.out if out is None else self._check_out(out)
         if self.exchange is not None:
             _lib.check(_lib.lib.fgc_exchange_average(self.plan.handle, self.exchange.handle, grad.data_ptr(), code,
                                                      self.weights.ctypes.data, dst.data_ptr(), self.flags.data_ptr(),
@@ -202,7 +233,8 @@ class GradientAverager:
                                                   D.stream()))
         return dst
 
-    def step_host(self, grad: torch.Tensor, out: torch.Tensor | None = None, wait: bool = True) -> torch.Tensor:
+    def step_host(self, grad: torch.Tensor, out: torch.Tensor | None = None, wait: bool = True,
+                  theta: float | None = None) -> torch.Tensor:
         """The averaging step from and to host memory: the PCIe copies of the
         gradient and of the average overlap the codec kernels piece by piece
         (fgc_average_host).  Pass pinned CPU tensors for the overlap.  With
@@ -215,8 +247,10 @@ class GradientAverager:
         code = _lib.DTYPE_F64 if grad.dtype == torch.float64 else _lib.DTYPE_F32
         grad = grad.contiguous()
         dst = out if out is not None else torch.empty(self.n, dtype=torch.float32, pin_memory=True)
-        if dst.is_cuda or dst.numel() != self.n or dst.dtype != torch.float32:
-            raise ValueError("out must be a float32 host tensor of the planned length")
+        if dst.is_cuda or dst.numel() != self.n or dst.dtype != torch.float32 or not dst.is_contiguous():
+            raise ValueError("out must be a contiguous float32 host tensor of the planned length")
+        if theta is not None:
+            self.set_theta(theta)
         dg = getattr(self, "_dgrad", None)
         if dg is None or dg.dtype != grad.dtype:
             dg = self._dgrad = torch.empty(self.n, dtype=grad.dtype, device=self.out.device)

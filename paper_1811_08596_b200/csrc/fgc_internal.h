@@ -205,6 +205,9 @@ fgc_status launch_message_unpack(const ChunkInfo* d_chunks, uint32_t n_chunks, c
 fgc_status launch_message_pack(const ChunkInfo* d_chunks, uint32_t n_chunks, const uint8_t* flags01,
                                const uint32_t* codes, const uint64_t* code_offsets, int n_bits, uint8_t* message,
                                uint32_t* popcounts, uint32_t* flags, cudaStream_t s);
+// Runtime theta (fgc_plan_set_theta): chunk c's drop count becomes
+// min(ceil(theta * bins), bins) in float64 (spectral.py:131), on the stream.
+fgc_status launch_set_drop(ChunkInfo* d_chunks, uint32_t n_chunks, double theta, cudaStream_t s);
 fgc_status launch_scan_u64(uint64_t* v, uint32_t n, uint64_t* total, uint64_t add, cudaStream_t s);
 
 // Fused sm_100a kernels for 65536-sample chunks (fused.cu).
@@ -243,6 +246,11 @@ fgc_status exchange_events(fgc_exchange* x, uint32_t P, std::vector<cudaEvent_t>
 void exchange_counters(fgc_exchange* x, uint32_t** counter, uint64_t** step, int* nranks, int* rank,
                        uint64_t* msg_bytes);
 bool exchange_ready(const fgc_exchange* x);
+// A step that failed after it began enqueueing pushes / flag writes leaves the
+// peers' counters out of step with ours: poison the exchange so every later
+// call fails fast instead of waiting forever.
+void exchange_poison(fgc_exchange* x);
+bool exchange_poisoned(const fgc_exchange* x);
 void exchange_trace(cudaStream_t s, const char* tag);
 
 }  // namespace fgc

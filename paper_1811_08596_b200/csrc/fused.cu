@@ -885,7 +885,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       for (;;) {
         uint32_t v;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-        if (v == a.pw.tag) break;
+        if ((int32_t)(v - a.pw.tag) >= 0) break;      // wraparound-safe: tags only grow
         __nanosleep(256);
       }
     }

@@ -52,6 +52,7 @@ using namespace fgc;
 
 struct fgc_plan {
   fgc_codec_desc desc{};
+  double theta_cap = 0.0;            // count mode: the theta message capacity is sized for
   QuantParams q{};
   uint32_t n_chunks = 0;
   std::vector<ChunkInfo> chunks;
@@ -153,6 +154,7 @@ extern "C" fgc_status fgc_plan_create(const fgc_codec_desc* desc, fgc_plan** out
   }
   fgc_plan* p = new fgc_plan();
   p->desc = dd;
+  p->theta_cap = dd.theta;
   p->q = make_qparams(p->desc);
   const int N = p->q.n_bits;
   const uint64_t full = d.n / d.chunk_size;
@@ -287,6 +289,27 @@ extern "C" void fgc_plan_destroy(fgc_plan* p) {
   for (cudaEvent_t e : p->ev_gath) cudaEventDestroy(e);
   if (p->xstream) cudaStreamDestroy(p->xstream);
   delete p;
+}
+
+extern "C" fgc_status fgc_plan_set_theta(fgc_plan* p, double theta, void* stream) {
+  if (!p) { set_error("null argument"); return FGC_ERR_INVALID; }
+  if (!(theta >= 0.0 && theta <= 1.0)) { set_error("theta must be in [0, 1]"); return FGC_ERR_INVALID; }
+  if (p->desc.mode == FGC_MODE_COUNT && !p->desc.full_capacity && theta < p->theta_cap) {
+    set_error("theta " + std::to_string(theta) + " is below the plan's capacity theta " +
+              std::to_string(p->theta_cap));
+    return FGC_ERR_INVALID;
+  }
+  if (theta == p->desc.theta) return FGC_OK;
+  p->desc.theta = theta;
+  bool changed = false;
+  for (ChunkInfo& ci : p->chunks) {
+    const double kd = ceil(theta * (double)ci.bins);
+    const uint32_t drop = (uint32_t)std::min<double>(kd, (double)ci.bins);
+    changed |= drop != ci.drop;
+    ci.drop = drop;
+  }
+  if (!changed) return FGC_OK;
+  return launch_set_drop(p->d_chunks, p->n_chunks, theta, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" fgc_status fgc_plan_get_info(const fgc_plan* p, fgc_plan_info* out) {
@@ -594,6 +617,16 @@ extern "C" fgc_status fgc_wire_index(const uint8_t* w, uint64_t len, const fgc_c
     const uint64_t cb = ((uint64_t)k * N + 7) / 8;
     if (pos + cb > len) {
       *n_valid = (uint32_t)c;   // bitmap of chunk c is present; its codes are not
+      // the reference checks the bitmap popcount against `kept` before the
+      // code bytes (codec.py:424-433): chunk c's bitmap decides the error class
+      uint64_t pop = 0;
+      const uint8_t* b = w + pos - bmb;
+      for (uint64_t i = 0; i < slots / 8; ++i) pop += (uint64_t)__builtin_popcount(b[i]);
+      if (slots % 8) pop += (uint64_t)__builtin_popcount(b[slots / 8] >> (8 - slots % 8));
+      if (pop != k) {
+        set_error("bitmap marks " + std::to_string(pop) + " slots, header says " + std::to_string(k));
+        return FGC_ERR_BITMAP;
+      }
       set_error("buffer ended inside the packed codes");
       return FGC_ERR_TRUNCATED;
     }
@@ -749,10 +782,29 @@ static std::vector<uint32_t> wave_pieces(const fgc_plan* p, uint32_t waves) {
   return f;
 }
 
+static fgc_status exchange_not_ready(const fgc_exchange* x) {
+  set_error(exchange_poisoned(x) ? "exchange poisoned: an earlier step failed after it began publishing"
+                                 : "exchange not opened");
+  return FGC_ERR_INVALID;
+}
+
+static fgc_status exchange_average_impl(fgc_plan* p, fgc_exchange* x, const void* grad, int dtype,
+                                        const double* weights, float* out, uint32_t* flags, void* stream,
+                                        bool* started);
+
 extern "C" fgc_status fgc_exchange_average(fgc_plan* p, fgc_exchange* x, const void* grad, int dtype,
                                            const double* weights, float* out, uint32_t* flags, void* stream) {
+  bool started = false;
+  const fgc_status st = exchange_average_impl(p, x, grad, dtype, weights, out, flags, stream, &started);
+  if (st != FGC_OK && started) exchange_poison(x);
+  return st;
+}
+
+static fgc_status exchange_average_impl(fgc_plan* p, fgc_exchange* x, const void* grad, int dtype,
+                                        const double* weights, float* out, uint32_t* flags, void* stream,
+                                        bool* started) {
   if (!p || !x || !grad || !out || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
-  if (!exchange_ready(x)) { set_error("exchange not opened"); return FGC_ERR_INVALID; }
+  if (!exchange_ready(x)) return exchange_not_ready(x);
   FGC_TRY(check_mode(p));
   FGC_TRY(check_signal(grad, dtype));
   uint32_t* counter;
@@ -772,6 +824,7 @@ extern "C" fgc_status fgc_exchange_average(fgc_plan* p, fgc_exchange* x, const v
   const uint32_t Pmax = exchange_max_pieces();
   uint8_t *message, *gathered;
   FGC_TRY(fgc_exchange_message(x, k, &message, &gathered));
+  *started = true;
   exchange_trace(s, "start");
   if (p->desc.mode == FGC_MODE_ENERGY) {
     // energy mode: no fused chunks; the whole message is one piece
@@ -850,9 +903,23 @@ extern "C" fgc_status fgc_exchange_average(fgc_plan* p, fgc_exchange* x, const v
 // device->host copy overlaps the next pieces.  The generic (tail) chunks are
 // copied in first and run their longer kernel chain on the side stream, off
 // the critical path of the last piece.
+static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* host_grad, int dtype,
+                                    const double* weights, void* dev_grad, uint8_t* message, float* dev_out,
+                                    float* host_out, uint32_t* flags, void* stream, bool* started);
+
 extern "C" fgc_status fgc_average_host(fgc_plan* p, fgc_exchange* x, const void* host_grad, int dtype,
                                        const double* weights, void* dev_grad, uint8_t* message, float* dev_out,
                                        float* host_out, uint32_t* flags, void* stream) {
+  bool started = false;
+  const fgc_status st = average_host_impl(p, x, host_grad, dtype, weights, dev_grad, message, dev_out, host_out,
+                                          flags, stream, &started);
+  if (st != FGC_OK && started && x) exchange_poison(x);
+  return st;
+}
+
+static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* host_grad, int dtype,
+                                    const double* weights, void* dev_grad, uint8_t* message, float* dev_out,
+                                    float* host_out, uint32_t* flags, void* stream, bool* started) {
   if (!p || !host_grad || !dev_grad || !dev_out || !host_out || !flags) {
     set_error("null argument");
     return FGC_ERR_INVALID;
@@ -865,7 +932,7 @@ extern "C" fgc_status fgc_average_host(fgc_plan* p, fgc_exchange* x, const void*
   uint64_t* step = nullptr;
   uint64_t mb = p->msg_bytes;
   if (x) {
-    if (!exchange_ready(x)) { set_error("exchange not opened"); return FGC_ERR_INVALID; }
+    if (!exchange_ready(x)) return exchange_not_ready(x);
     exchange_counters(x, &counter, &step, &W, &me, &mb);
     if (mb != p->msg_bytes) { set_error("exchange sized for another plan"); return FGC_ERR_INVALID; }
   } else if (!message) {
@@ -901,6 +968,7 @@ extern "C" fgc_status fgc_average_host(fgc_plan* p, fgc_exchange* x, const void*
     tval = (uint32_t)(*step + 1);
     FGC_TRY(fgc_exchange_message(x, k, &message, &gathered));
   }
+  *started = true;
   const size_t esz = dtype == FGC_DTYPE_F64 ? 8 : 4;
   auto h2d = [&](uint64_t lo, uint64_t hi) {
     return cudaMemcpyAsync(static_cast<uint8_t*>(dev_grad) + lo * esz, static_cast<const uint8_t*>(host_grad) + lo * esz,

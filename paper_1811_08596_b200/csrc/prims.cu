@@ -297,6 +297,23 @@ extern "C" fgc_status fgc_irfft(const void* spectrum, uint64_t L, double* signal
   return FGC_OK;
 }
 
+namespace fgc {
+__global__ void k_set_drop(ChunkInfo* chunks, uint32_t n, double theta) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const uint32_t bins = chunks[c].bins;
+  const double kd = ceil(theta * (double)bins);             // IEEE-RN product, exact ceil: as on the host
+  chunks[c].drop = kd >= (double)bins ? bins : (uint32_t)kd;
+}
+
+fgc_status launch_set_drop(ChunkInfo* d_chunks, uint32_t n_chunks, double theta, cudaStream_t s) {
+  if (!n_chunks) return FGC_OK;
+  k_set_drop<<<(n_chunks + 255) / 256, 256, 0, s>>>(d_chunks, n_chunks, theta);
+  FGC_LAUNCHED(1);
+  return FGC_OK;
+}
+}  // namespace fgc
+
 static fgc_status truncate_impl(const void* spectrum, uint64_t bins, uint64_t n, double theta, int mode, void* out,
                                 uint8_t* kept_mask, void* stream) {
   if (!spectrum || !out || !kept_mask || bins < 1 || bins > 0x7FFFFFFFull) return FGC_ERR_INVALID;

@@ -98,6 +98,7 @@ struct fgc_exchange {
   uint32_t pexp[kMaxPieces] = {};     // host copy of what pcnt[i] reaches once the queued compresses finish
   uint64_t step = 0;
   bool opened = false;
+  bool poisoned = false;              // a step failed mid-way: counters no longer agree with the peers
 };
 
 using fgc::set_error;
@@ -352,7 +353,11 @@ void exchange_counters(fgc_exchange* x, uint32_t** counter, uint64_t** step, int
   *msg_bytes = x->msg_bytes;
 }
 
-bool exchange_ready(const fgc_exchange* x) { return x && x->opened; }
+bool exchange_ready(const fgc_exchange* x) { return x && x->opened && !x->poisoned; }
+void exchange_poison(fgc_exchange* x) {
+  if (x) x->poisoned = true;
+}
+bool exchange_poisoned(const fgc_exchange* x) { return x && x->poisoned; }
 
 }  // namespace fgc
 

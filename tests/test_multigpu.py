@@ -35,38 +35,43 @@ def _worker(rank, world, port, n, transport, mode, out_q, theta=0.9, nm=(8, 3), 
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        rng = np.random.default_rng(77)
-        rows = (rng.standard_normal((world, n)) * 1e-2).astype(np.float32)
-        for c, scale in special:                # zero / tiny chunks on rank 0
-            rows[0, c * 65536:(c + 1) * 65536] *= scale
-        q = F.calibrate([rows[0]], *nm)
+        steps = 4
+        thetas = [theta, min(1.0, theta + 0.02), theta, min(1.0, theta + 0.05)]
+        rows = []                                # a different gradient on every step and rank
+        for s in range(steps):
+            rng = np.random.default_rng(77 + s)
+            r = (rng.standard_normal((world, n)) * 1e-2).astype(np.float32)
+            for c, scale in special:            # zero / tiny chunks on rank 0
+                r[0, c * 65536:(c + 1) * 65536] *= scale
+            rows.append(r)
+        q = F.calibrate([rows[0][0]], *nm)
         cfg = F.CodecConfig(F.SparsificationSpec(theta, mode), q)
         comm = NcclComm()
         w = F.shard_weights(5 * world + 1, world)
         avg = GradientAverager(n, cfg, w, comm, transport=transport)
-        g = torch.from_numpy(rows[rank]).cuda()
         outs = []
-        for _ in range(3):                      # the peer exchange alternates two gather buffers
-            outs.append(avg.step(g).clone())
-        hin = torch.from_numpy(rows[rank]).pin_memory()
-        for _ in range(2):                      # host-buffer step: same bits as the device step
-            hout = avg.step_host(hin)
-            assert torch.equal(hout, outs[0].cpu()), "host step disagrees"
-            outs.append(avg.step(g).clone())
+        for s in range(steps):                  # the peer exchange alternates two gather buffers
+            g = torch.from_numpy(rows[s][rank]).cuda()
+            outs.append(avg.step(g, theta=thetas[s]).clone())
+        for s in (1, 2):                        # host-buffer step: same bits as the device step
+            hout = avg.step_host(torch.from_numpy(rows[s][rank]).pin_memory(), theta=thetas[s])
+            assert torch.equal(hout, outs[s].cpu()), "host step disagrees"
         avg.check()
-        got = outs[0].double().cpu().numpy()
-        for o in outs[1:]:
-            assert torch.equal(o, outs[0]), "steps disagree"
         avg.close()
-        # oracle: decode every rank's message (the wire bytes of this rank's
-        # own compress are bit-identical on all ranks, so serialize locally)
-        msgs = [F.compress(rows[k], cfg) for k in range(world)]
-        ref = sum(w[k] * O.decompress(O.from_wire(F.serialize(msgs[k]))) for k in range(world))
-        # a coarse lattice can zero every code (eps above every coefficient): then got must be 0 too
-        rel = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30))
+        # oracle: decode every rank's message of every step (the wire bytes of a
+        # rank's compress are bit-identical on all ranks, so serialize locally)
+        rels = []
+        for s in range(steps):
+            scfg = F.CodecConfig(F.SparsificationSpec(thetas[s], mode), q)
+            msgs = [F.compress(rows[s][k], scfg) for k in range(world)]
+            ref = sum(w[k] * O.decompress(O.from_wire(F.serialize(msgs[k]))) for k in range(world))
+            got = outs[s].double().cpu().numpy()
+            # a coarse lattice can zero every code (eps above every coefficient): then got must be 0 too
+            rels.append(float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)))
         # every rank must hold bit-identical results
-        digest = float(np.frombuffer(got.tobytes(), dtype=np.uint64).astype(np.float64).sum())
-        out_q.put((rank, rel, digest))
+        digest = float(sum(np.frombuffer(o.cpu().numpy().tobytes(), dtype=np.uint32).astype(np.float64).sum()
+                           for o in outs))
+        out_q.put((rank, max(rels), digest))
         comm.close()
     finally:
         dist.destroy_process_group()

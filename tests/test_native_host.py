@@ -122,6 +122,40 @@ def test_wire_error_taxonomy_host_side(golden):
                                    C.byref(nv)) == _lib.ERR_FORMAT
 
 
+@pytest.mark.parametrize("delta", [1, -1, 7])
+def test_wire_kept_field_tampered(golden, delta):
+    """Raising or lowering a chunk's `kept` field: the reference compares the
+    bitmap popcount with `kept` before it looks at the code bytes
+    (codec.py:424-433), so the error class is the bitmap mismatch even when
+    the inflated code length also runs past the buffer."""
+    meta, _ = golden
+    kinds = {_lib.ERR_BITMAP: "bitmap", _lib.ERR_TRUNCATED: "truncated", _lib.ERR_FORMAT: "format"}
+    for rec in meta["fixtures"]:
+        blob = bytearray(bytes.fromhex(rec["hex"]))
+        kept = int.from_bytes(blob[36:40], "little")
+        if kept + delta < 0:
+            continue
+        blob[36:40] = (kept + delta).to_bytes(4, "little")
+        with pytest.raises(O.WireError) as exc:
+            O.from_wire(bytes(blob))
+        st, d = _parse(bytes(blob))
+        assert st == 0
+        n_chunks = len(O.chunk_lengths(d.n, d.chunk_size))
+        offs = np.zeros(n_chunks, dtype=np.uint64)
+        nnz = np.zeros(n_chunks, dtype=np.uint32)
+        nv = C.c_uint32()
+        st = _lib.lib.fgc_wire_index(bytes(blob), len(blob), C.byref(d), offs.ctypes.data, nnz.ctypes.data,
+                                     C.byref(nv))
+        # The host index checks the framing and, where chunk c's codes overrun
+        # the buffer, chunk c's bitmap; the popcounts of the chunks it could
+        # frame are the device deserializer's (tests/test_gpu_codec.py::
+        # test_wire_errors), which runs before a framing error is raised.
+        if st in (_lib.ERR_TRUNCATED, _lib.ERR_BITMAP):
+            assert kinds[st] == exc.value.kind, (st, exc.value.kind)
+        if exc.value.kind == "bitmap" and nv.value == 0:
+            assert st == _lib.ERR_BITMAP
+
+
 def test_compression_ratio_paper_setting():
     q = F.tune_eps(-1.0, 1.0, 8, 3)
     cfg = F.CodecConfig(F.SparsificationSpec(0.7), q)

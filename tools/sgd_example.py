@@ -8,8 +8,9 @@ Each rank owns a shard of a synthetic least-squares problem
 f(x) = 1/(2m) ||A x - b||^2 over its rows; per step it computes its shard
 gradient on the GPU, the GradientAverager averages the W compressed
 gradients (compress -> peer exchange -> frequency-domain weighted decode),
-and every rank applies the identical update.  The codec plan is rebuilt only
-when theta changes (plans are cached).
+and every rank applies the identical update.  One averager (one plan, one
+peer exchange) serves the whole schedule: its messages are sized for
+capacity_theta = 0 and every step passes its theta at run time.
 
     torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/sgd_example.py --iters 200
     python tools/sgd_example.py --iters 200            # single GPU
@@ -69,7 +70,7 @@ def main():
     w = shard_weights(world * a.rows, world)
     x = torch.zeros(a.dim, device=dev)
     q = None
-    averagers = {}
+    avg = None
     trace = []
     for t in range(a.iters):
         eta = eta0 / (1.0 + t / a.tau) ** a.power
@@ -77,17 +78,16 @@ def main():
         g = A.T @ (A @ x - b) / a.rows
         if q is None:                                   # range fixed from the first gradient (simulator.py:354)
             q = F.calibrate([g], a.nbits, a.mantissa)
-        key = round(theta, 6)
-        if key not in averagers:
-            averagers[key] = GradientAverager(a.dim, F.CodecConfig(F.SparsificationSpec(key), q), w, comm)
-        v_hat = averagers[key].step(g)
+        if avg is None:
+            avg = GradientAverager(a.dim, F.CodecConfig(F.SparsificationSpec(theta), q), w, comm,
+                                   capacity_theta=0.0)
+        v_hat = avg.step(g, theta=theta)
         x = x - eta * v_hat
         if t % 20 == 0 or t == a.iters - 1:
             loss = float(((A @ x - b) ** 2).mean() / 2)
             trace.append({"t": t, "theta": theta, "eta": eta, "shard_loss": loss})
-    for avg in averagers.values():
-        avg.check()
-        avg.close()
+    avg.check()
+    avg.close()
     if rank == 0:
         print(json.dumps({"world": world, "dim": a.dim, "L": L, "trace": trace}), flush=True)
     if comm is not None:
