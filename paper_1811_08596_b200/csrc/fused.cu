@@ -800,6 +800,7 @@ struct DecodeArgs {
 };
 
 constexpr int kDecBatch = 4;                           // messages per block scan in the decode
+constexpr uint32_t kDecStageWords = 8192;              // code words of a message batch staged in smem
 
 struct __align__(16) DecodeShared {
   float2 x[kPadded + 64];            // this CTA's bins of the weighted spectrum sum, then Y_r / FFT scratch
@@ -808,7 +809,12 @@ struct __align__(16) DecodeShared {
   uint32_t bm[kDecBatch][2 * kThreads * 2];   // natural-order bitmap words 0..2047 of a message batch
   uint32_t pref[kDecBatch][2 * kThreads];     // codes before each 32-bin block
   uint32_t bmN[kDecBatch];                    // word 2048 (bin N)
+  uint32_t soff[kDecBatch];                   // staging offset (words) of each message, ~0u: not staged
   uint32_t scan[4 * (kThreads / 32 + 1)];     // block_exclusive_scan4 scratch
+  // packed code streams of the batch's messages (whole chunk segments, each
+  // 16-byte aligned), copied once with coalesced loads so the per-lane bit
+  // walk refills its window from shared memory instead of L2
+  uint4 stage[kDecStageWords / 4 + 2];
 };
 
 // decode, one cluster of 2 CTAs per chunk.
@@ -930,8 +936,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     FGC_TS(0);
     for (int w0 = 0; w0 < a.W; w0 += kDecBatch) {
       const int G = min(kDecBatch, a.W - w0);
-      // 1a. every bitmap word of the batch (thread t: blocks 2t, 2t+1), block code prefixes
+      // 1a. every bitmap word of the batch (thread t: blocks 2t, 2t+1), block code prefixes;
+      //     the code streams of the messages that fit are staged in smem meanwhile
       uint32_t cnt2[kDecBatch][2];
+      uint32_t soff[kDecBatch];                 // staging offset in words, or ~0u: read from global
+      {
+        uint32_t used_total = 0;
+#pragma unroll
+        for (int i = 0; i < kDecBatch; ++i) {
+          soff[i] = ~0u;
+          if (tid == 0) sh.soff[i] = ~0u;
+          if (i < G) {
+            const uint8_t* sg = a.messages + (uint64_t)(w0 + i) * a.stride + ci.seg_off;
+            const uint32_t nnz = __ldg(reinterpret_cast<const uint32_t*>(sg));
+            const uint32_t used4 = (uint32_t)min((((uint64_t)nnz * N + 127u) >> 7), (uint64_t)((ci.code_cap + 3u) >> 2));
+            if (!(dbg & 4u) && used_total + 4u * used4 <= kDecStageWords) {
+              soff[i] = used_total;
+              if (tid == 0) sh.soff[i] = used_total;
+              const uint4* src = reinterpret_cast<const uint4*>(sg + ci.code_off);
+              for (uint32_t e = tid; e < used4; e += kThreads) sh.stage[(used_total >> 2) + e] = __ldg(src + e);
+              used_total += 4u * used4;
+            }
+          }
+        }
+      }
 #pragma unroll
       for (int i = 0; i < kDecBatch; ++i) {
         cnt2[i][0] = cnt2[i][1] = 0u;
@@ -961,60 +989,98 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       }
       __syncthreads();
       if (w0 == 0) FGC_TS(7);
-      // 1b. my block's slots; the first code words of every message of the batch are loaded together
-      uint32_t wd[kDecBatch][3], idx[kDecBatch], win[kDecBatch][4], wbase[kDecBatch];
-      const uint32_t* cwp[kDecBatch];
-#pragma unroll
-      for (int i = 0; i < kDecBatch; ++i) {
-        wd[i][0] = wd[i][1] = wd[i][2] = 0u;
-        idx[i] = 0u;
-        wbase[i] = 0u;
-        cwp[i] = nullptr;
-        if (i < G) {
-          wd[i][0] = sh.bm[i][2 * blk];
-          wd[i][1] = sh.bm[i][2 * blk + 1];
-          if (binN) wd[i][2] = sh.bmN[i];
-          idx[i] = sh.pref[i][blk];
-          cwp[i] = reinterpret_cast<const uint32_t*>(a.messages + (uint64_t)(w0 + i) * a.stride + ci.seg_off +
-                                                     ci.code_off);
-          wbase[i] = (idx[i] * N) >> 5;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          win[i][q] = 0u;
-          if (i < G && (wd[i][0] | wd[i][1] | wd[i][2]) && wbase[i] + q < ci.code_cap)
-            win[i][q] = __ldg(cwp[i] + wbase[i] + q);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < kDecBatch; ++i) {
-        if (i >= G) break;
-        const float wt = a.wts.w[w0 + i];
-        // codes are consumed in stream order: a 4-word window that slides by one word
-        uint32_t A = win[i][0], B = win[i][1], C = win[i][2], D = win[i][3];
-        uint32_t o = (idx[i] * N) & 31u, nxt = wbase[i] + 4u;
+      // 1b. my block's slots, message by message in worker order (single
+      //     writer per slot: deterministic).  Staged messages read their codes
+      //     from shared memory by code index (N = 8 / 16: one byte / halfword
+      //     load), the others through a register window over global memory.
+      {
         const uint32_t mask = (1u << N) - 1u;
-        auto run = [&](uint64_t m64, float* basef) {   // slot s of the block is float s of its entries
-          while (m64) {
-            const uint32_t pos = __ffsll((long long)m64) - 1;
-            m64 &= m64 - 1;
-            const uint32_t c = __funnelshift_r(A, B, o) & mask;
-            o += N;
-            if (o >= 32u) {
-              o -= 32u;
-              A = B; B = C; C = D;
-              D = nxt < ci.code_cap ? __ldg(cwp[i] + nxt) : 0u;
-              ++nxt;
-            }
-            // decode_code (quantizer.py:239-253) without branches
-            const bool neg = c > a.q.npos;
-            const uint32_t e = a.q.pbase + c - 1u - (neg ? a.q.npos : 0u);
-            const float v = __uint_as_float((e << a.q.shift) | (neg ? 0x80000000u : 0u));
-            basef[pos] += (c ? v : 0.0f) * wt;
-          }
+        float* minef = reinterpret_cast<float*>(mine);
+        float* nf = reinterpret_cast<float*>(acc + pad(kHalfBins));
+        const QuantParams& qq = a.q;
+        auto add = [&](float* f, uint32_t pos, uint32_t c, float wt) {
+          // decode_code (quantizer.py:239-253) without branches
+          const bool neg = c > qq.npos;
+          const uint32_t e = qq.pbase + c - 1u - (neg ? qq.npos : 0u);
+          const float v = __uint_as_float((e << qq.shift) | (neg ? 0x80000000u : 0u));
+          f[pos] += (c ? v : 0.0f) * wt;
         };
-        run(((uint64_t)wd[i][1] << 32) | wd[i][0], reinterpret_cast<float*>(mine));
-        if (binN) run(wd[i][2], reinterpret_cast<float*>(acc + pad(kHalfBins)));
+#pragma unroll 1
+        for (int i = 0; i < G; ++i) {
+          const uint32_t m0 = sh.bm[i][2 * blk], m1 = sh.bm[i][2 * blk + 1], m2 = binN ? sh.bmN[i] : 0u;
+          if (!(m0 | m1 | m2)) continue;
+          const float wt = a.wts.w[w0 + i];
+          uint32_t k = sh.pref[i][blk];                       // stream index of my first code
+          const uint32_t so = sh.soff[i];
+          if (so != ~0u && N == 8) {
+            const uint8_t* s8 = reinterpret_cast<const uint8_t*>(sh.stage) + 4u * so;
+            auto walk = [&](uint32_t m, float* f) {
+              while (m) {
+                const uint32_t pos = __ffs(m) - 1;
+                m &= m - 1;
+                add(f, pos, s8[k++], wt);
+              }
+            };
+            walk(m0, minef);
+            walk(m1, minef + 32);
+            walk(m2, nf);
+          } else if (so != ~0u && N == 16) {
+            const uint16_t* s16 = reinterpret_cast<const uint16_t*>(sh.stage) + 2u * so;
+            auto walk = [&](uint32_t m, float* f) {
+              while (m) {
+                const uint32_t pos = __ffs(m) - 1;
+                m &= m - 1;
+                add(f, pos, s16[k++], wt);
+              }
+            };
+            walk(m0, minef);
+            walk(m1, minef + 32);
+            walk(m2, nf);
+          } else if (so != ~0u) {
+            const uint32_t* st = reinterpret_cast<const uint32_t*>(sh.stage) + so;
+            uint32_t bit = k * N;
+            auto walk = [&](uint32_t m, float* f) {
+              while (m) {
+                const uint32_t pos = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t wi = bit >> 5;
+                add(f, pos, __funnelshift_r(st[wi], st[wi + 1], bit & 31u) & mask, wt);
+                bit += N;
+              }
+            };
+            walk(m0, minef);
+            walk(m1, minef + 32);
+            walk(m2, nf);
+          } else {
+            // codes from global memory through a 4-word register window
+            const uint32_t* cw = reinterpret_cast<const uint32_t*>(a.messages + (uint64_t)(w0 + i) * a.stride +
+                                                                   ci.seg_off + ci.code_off);
+            const uint32_t wb = (k * N) >> 5;
+            uint32_t A = wb < ci.code_cap ? __ldg(cw + wb) : 0u;
+            uint32_t B = wb + 1 < ci.code_cap ? __ldg(cw + wb + 1) : 0u;
+            uint32_t C = wb + 2 < ci.code_cap ? __ldg(cw + wb + 2) : 0u;
+            uint32_t D = wb + 3 < ci.code_cap ? __ldg(cw + wb + 3) : 0u;
+            uint32_t o = (k * N) & 31u, nxt = wb + 4u;
+            auto walk = [&](uint32_t m, float* f) {
+              while (m) {
+                const uint32_t pos = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t c = __funnelshift_r(A, B, o) & mask;
+                o += N;
+                if (o >= 32u) {
+                  o -= 32u;
+                  A = B; B = C; C = D;
+                  D = nxt < ci.code_cap ? __ldg(cw + nxt) : 0u;
+                  ++nxt;
+                }
+                add(f, pos, c, wt);
+              }
+            };
+            walk(m0, minef);
+            walk(m1, minef + 32);
+            walk(m2, nf);
+          }
+        }
       }
       if (w0 == 0) FGC_TS(8);
       __syncthreads();                                      // bm / pref reusable

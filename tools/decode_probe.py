@@ -10,6 +10,9 @@ from paper_1811_08596_b200 import _lib, _device as D
 from paper_1811_08596_b200.codec import _compress_device
 
 torch.cuda.set_device(0)
+import ctypes, os
+if os.environ.get("FGC_KNOBS"):
+    _lib.lib.fgc_debug_set_fused_knobs(ctypes.c_uint32(int(os.environ["FGC_KNOBS"])))
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 25_600_000
 Ws = [int(x) for x in sys.argv[2:]] or [1, 2, 4, 8]
 q = F.tune_eps(-200.0, 200.0, 8, 3)
