@@ -224,6 +224,12 @@ fgc_status launch_fused_compress(const FusedTables* t, const ChunkInfo* d_chunks
 fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
                                const QuantParams& q, float* out, cudaStream_t s, PieceWait pw = PieceWait());
+// 4-CTA-cluster compress, two CTAs per SM (fused4.cu); thi / tlo are the
+// fused kernels' twiddle tables, `ahead` the L2 prefetch distance in chunks.
+fgc_status launch_compress4(const float2* thi, const float2* tlo, uint32_t ahead, const ChunkInfo* d_chunks,
+                            uint32_t first, uint32_t count, const void* grad, int dtype, int half_pass,
+                            const QuantParams& q, uint8_t* message, uint32_t* flags, float2* fb_spec, float2* dbg,
+                            cudaStream_t s, PieceCounter pc);
 // Debug hooks: the fused kernels' own forward coefficients / inverse.
 fgc_status launch_fused_spectrum(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                  const void* grad, int dtype, int half_pass, float2* spectrum, uint32_t* flags,

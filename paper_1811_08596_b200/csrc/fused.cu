@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
@@ -1189,6 +1190,7 @@ bool fused_available() { return true; }
 extern "C" int fgc_debug_set_fused_knobs(uint32_t knobs) {
   return cudaMemcpyToSymbol(fgc::g_fused_dbg, &knobs, sizeof(knobs)) == cudaSuccess ? 0 : 1;
 }
+extern "C" int fgc_debug_set_compress_kernel(int k);
 extern "C" int fgc_debug_fused_timestamps(unsigned long long* host, uint32_t count) {
   if (count > 2048 * 16) count = 2048 * 16;
   return cudaMemcpyFromSymbol(host, fgc::g_fused_ts, count * sizeof(unsigned long long)) == cudaSuccess ? 0 : 1;
@@ -1239,11 +1241,28 @@ void fused_tables_free(FusedTables* t) {
   delete t;
 }
 
+// Which compress kernel runs the 65536-sample chunks: 2 = k_fused_compress
+// above (default), 4 = the 4-CTA-cluster kernel of fused4.cu (two CTAs per
+// SM; bit-identical messages, measured slower: 226 vs 185 us at 25.6M floats,
+// its cluster barriers across 4 CTAs on shared SMs stall ~39% of the time).
+// FGC_COMPRESS_KERNEL sets the default; fgc_debug_set_compress_kernel switches it.
+static int g_compress_kernel = -1;
+static int compress_kernel() {
+  if (g_compress_kernel < 0) {
+    const char* e = getenv("FGC_COMPRESS_KERNEL");
+    g_compress_kernel = (e && e[0] == '4') ? 4 : 2;
+  }
+  return g_compress_kernel;
+}
+
 static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first,
                                        uint32_t count, const void* grad, int dtype, int half_pass,
                                        const QuantParams& q, uint8_t* message, uint32_t* flags,
                                        float2* fb_spec, float2* dbg, cudaStream_t s, PieceCounter pc) {
   if (!count) return FGC_OK;
+  if (compress_kernel() == 4)
+    return launch_compress4(t->thi, t->tlo, t->wave, d_chunks, first, count, grad, dtype, half_pass, q, message,
+                            flags, fb_spec, dbg, s, pc);
   CompressArgs a{d_chunks, first, grad, q, message, flags, t->thi, t->tlo, t->t1024, fb_spec, dbg, count, t->wave,
                  pc};
   const size_t smem = sizeof(CompressShared);
@@ -1328,3 +1347,8 @@ fgc_status launch_fused_inverse(const FusedTables* t, const ChunkInfo* d_chunks,
 }
 
 }  // namespace fgc
+
+extern "C" int fgc_debug_set_compress_kernel(int k) {
+  fgc::g_compress_kernel = (k == 4) ? 4 : 2;
+  return 0;
+}

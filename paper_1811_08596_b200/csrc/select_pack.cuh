@@ -1,5 +1,5 @@
 // Generic count-mode selection + quantize + pack of ONE chunk by one CTA of
-// kSelThreads threads, from coefficients in global memory.  Shared by the
+// TH threads (default kSelThreads), from coefficients in global memory.  Shared by the
 // generic kernel (codec_generic.cu) and the fused compress kernel, which
 // hands a degenerate chunk to it in place (fused.cu).
 //
@@ -22,11 +22,12 @@ constexpr int kCandCap = 1024;
 constexpr uint32_t kHistBins = 2048;
 
 constexpr int kPer = 4;                                   // bins per thread per final-pass tile
-constexpr uint32_t kTile = kPer * kSelThreads;
-constexpr uint32_t kStageWords = 2 * kTile + 4;           // one tile of codes (<= 2 kTile codes * 32 bits)
 static_assert(16 % kPer == 0 || kPer == 16, "a lane group owns whole bitmap words");
 
-struct SelectShared {
+template <int TH>
+struct SelectSharedT {
+  static constexpr uint32_t kTile = kPer * TH;
+  static constexpr uint32_t kStageWords = 2 * kTile + 4;  // one tile of codes (<= 2 kTile codes * 32 bits)
   uint32_t hist[kHistBins];
   uint32_t scan[40];
   unsigned long long key[kCandCap];
@@ -35,6 +36,7 @@ struct SelectShared {
   uint32_t cnt;
   uint32_t found_bucket, found_below;
 };
+using SelectShared = SelectSharedT<kSelThreads>;
 
 template <typename CT>
 struct Coeffs;
@@ -58,32 +60,33 @@ struct Coeffs<double2> {
 // Visit every bin of the chunk, each thread kFly bins per round with their
 // loads issued together (the passes are latency-bound on these loads otherwise).
 constexpr int kFly = 4;
-template <typename CT, typename F>
+template <int TH, typename CT, typename F>
 __device__ __forceinline__ void for_bins(const Coeffs<CT>& cf, uint32_t B, F&& f) {
-  for (uint32_t i0 = threadIdx.x; i0 < B; i0 += kFly * kSelThreads) {
+  for (uint32_t i0 = threadIdx.x; i0 < B; i0 += kFly * TH) {
     float re[kFly], im[kFly];
     double dr[kFly], di[kFly];
 #pragma unroll
     for (int u = 0; u < kFly; ++u) {
-      const uint32_t i = i0 + u * kSelThreads;
+      const uint32_t i = i0 + u * TH;
       if (i < B) cf.get(i, re[u], im[u], dr[u], di[u]);
     }
 #pragma unroll
     for (int u = 0; u < kFly; ++u) {
-      const uint32_t i = i0 + u * kSelThreads;
+      const uint32_t i = i0 + u * TH;
       if (i < B) f(i, re[u], im[u], dr[u], di[u]);
     }
   }
 }
 
 // Bucket b such that below(b) <= r < below(b) + hist[b]; every thread returns it.
-__device__ void find_bucket(SelectShared& sh, uint32_t r, uint32_t& bucket, uint32_t& below) {
-  constexpr uint32_t per = kHistBins / kSelThreads;   // 4
+template <int TH>
+__device__ void find_bucket(SelectSharedT<TH>& sh, uint32_t r, uint32_t& bucket, uint32_t& below) {
+  constexpr uint32_t per = kHistBins / TH;            // 4 (512 threads) or 8 (256)
   uint32_t local = 0;
 #pragma unroll
   for (uint32_t q = 0; q < per; ++q) local += sh.hist[threadIdx.x * per + q];
   uint32_t total;
-  uint32_t before = block_exclusive_scan<kSelThreads>(local, sh.scan, total);
+  uint32_t before = block_exclusive_scan<TH>(local, sh.scan, total);
   if (r >= before && r < before + local) {
     uint32_t acc = before;
     for (uint32_t q = 0; q < per; ++q) {
@@ -107,7 +110,8 @@ __device__ __forceinline__ bool key_less(unsigned long long ka, uint32_t ia, uns
 }
 
 // Bitonic sort of the first M (power of two) entries by (key, idx) or by idx.
-__device__ void bitonic(SelectShared& sh, uint32_t M, bool by_index) {
+template <int TH>
+__device__ void bitonic(SelectSharedT<TH>& sh, uint32_t M, bool by_index) {
   for (uint32_t k = 2; k <= M; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
       for (uint32_t t = threadIdx.x; t < M; t += blockDim.x) {
@@ -132,9 +136,9 @@ enum SelMode : int { kKeepAll = 0, kDropAll = 1, kList = 2, kExact = 3, kMask = 
 
 
 // Select + pack chunk `ci` whose coefficients start at cf.p.  Every thread of
-// the CTA (kSelThreads) calls it; `sh` is the CTA's scratch.
-template <typename CT>
-__device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo ci, Coeffs<CT> cf, int exact_only,
+// the CTA (TH threads) calls it; `sh` is the CTA's scratch.
+template <typename CT, int TH = kSelThreads>
+__device__ __noinline__ void select_pack_chunk(SelectSharedT<TH>& sh, const ChunkInfo ci, Coeffs<CT> cf, int exact_only,
                                                const QuantParams q, uint8_t* message, uint8_t* kept_mask,
                                                uint32_t* flags, const uint8_t* drop_mask) {
   const uint32_t B = ci.bins;
@@ -158,18 +162,18 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
     } else {
       const uint32_t r = kdrop - 1;             // rank of the largest dropped bin
       // pass 1: proxy bits [30:20]
-      for (uint32_t b = tid; b < kHistBins; b += kSelThreads) sh.hist[b] = 0;
+      for (uint32_t b = tid; b < kHistBins; b += TH) sh.hist[b] = 0;
       __syncthreads();
-      for_bins(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
+      for_bins<TH>(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
         atomicAdd(&sh.hist[__float_as_uint(proxy_key(re, im)) >> 20], 1u);
       });
       __syncthreads();
       uint32_t b1, below1;
       find_bucket(sh, r, b1, below1);
       // pass 2: proxy bits [19:9] inside bucket b1
-      for (uint32_t b = tid; b < kHistBins; b += kSelThreads) sh.hist[b] = 0;
+      for (uint32_t b = tid; b < kHistBins; b += TH) sh.hist[b] = 0;
       __syncthreads();
-      for_bins(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
+      for_bins<TH>(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
         const uint32_t pb = __float_as_uint(proxy_key(re, im));
         if ((pb >> 20) == b1) atomicAdd(&sh.hist[(pb >> 9) & 0x7FFu], 1u);
       });
@@ -190,7 +194,7 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
     if (tid == 0) sh.cnt = 0;
     __syncthreads();
     uint32_t below_local = 0;
-    for_bins(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
+    for_bins<TH>(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
       const float p = proxy_key(re, im);
       if (!all_band && p < band_lo) {
         ++below_local;
@@ -199,13 +203,13 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
         if (s < kCandCap) sh.idx[s] = i;
       }
     });
-    const uint32_t below = block_sum<kSelThreads>(below_local, sh.scan);
+    const uint32_t below = block_sum<TH>(below_local, sh.scan);
     m = sh.cnt;
     need = kdrop - below;
     if (m <= (uint32_t)kCandCap) {
       uint32_t M = 1;
       while (M < m) M <<= 1;
-      for (uint32_t s = tid; s < M; s += kSelThreads) {
+      for (uint32_t s = tid; s < M; s += TH) {
         if (s < m) {
           float re, im; double dr, di;
           cf.get(sh.idx[s], re, im, dr, di);
@@ -217,7 +221,7 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
       }
       __syncthreads();
       bitonic(sh, M, false);
-      for (uint32_t s = tid; s < m; s += kSelThreads)
+      for (uint32_t s = tid; s < m; s += TH)
         if (s < need) sh.idx[s] |= 0x80000000u;  // mark dropped
       __syncthreads();
       bitonic(sh, M, true);
@@ -230,10 +234,10 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
       const int widths[6] = {11, 11, 11, 11, 11, 8};
       if (need > 0) {
         for (int pass = 0; pass < 6; ++pass) {
-          for (uint32_t b = tid; b < kHistBins; b += kSelThreads) sh.hist[b] = 0;
+          for (uint32_t b = tid; b < kHistBins; b += TH) sh.hist[b] = 0;
           __syncthreads();
           const unsigned long long dm = (1ull << widths[pass]) - 1ull;
-          for_bins(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
+          for_bins<TH>(cf, B, [&](uint32_t i, float re, float im, double dr, double di) {
             const float p = proxy_key(re, im);
             if (!(all_band || (p >= band_lo && p < band_hi))) return;
             const unsigned long long key = (unsigned long long)__double_as_longlong(cabs_key(dr, di));
@@ -254,7 +258,7 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
   }
 
   // ---- final pass: decide, quantize, bitmap + code stream.  Tiles of
-  //      kPer * kSelThreads bins, each thread kPer consecutive bins (so its
+  //      kPer * TH bins, each thread kPer consecutive bins (so its
   //      codes are consecutive in the stream and a lane pair owns one bitmap
   //      word); one block scan per tile places every thread's codes.
   uint32_t* seg = reinterpret_cast<uint32_t*>(message + ci.seg_off);
@@ -266,10 +270,10 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
   uint32_t origin = 0;        // global code word index of stage[0]
   uint32_t tie_seen = 0;
   bool overflow = false;
-  for (uint32_t s = tid; s < kStageWords; s += kSelThreads) sh.stage[s] = 0;
+  for (uint32_t s = tid; s < SelectSharedT<TH>::kStageWords; s += TH) sh.stage[s] = 0;
   __syncthreads();
 
-  for (uint32_t t0 = 0; t0 < B; t0 += kTile) {
+  for (uint32_t t0 = 0; t0 < B; t0 += SelectSharedT<TH>::kTile) {
     const uint32_t i0 = t0 + tid * kPer;
     float re[kPer], im[kPer];
     double dr[kPer], di[kPer];
@@ -315,7 +319,7 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
     }
     if (mode == kExact) {                        // ties dropped in bin order up to tie_cut
       uint32_t ties_total;
-      uint32_t tr = tie_seen + block_exclusive_scan<kSelThreads>(ntie, sh.scan, ties_total);
+      uint32_t tr = tie_seen + block_exclusive_scan<TH>(ntie, sh.scan, ties_total);
 #pragma unroll
       for (int u = 0; u < kPer; ++u)
         if (is_tie[u]) dropped[u] = tr++ < tie_cut;
@@ -342,10 +346,10 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
       }
     }
     uint32_t ttot;
-    const uint32_t r0 = rank_base + block_exclusive_scan<kSelThreads>(cnt, sh.scan, ttot);
+    const uint32_t r0 = rank_base + block_exclusive_scan<TH>(cnt, sh.scan, ttot);
     // stage the codes (LSB-first N-bit fields, bit 0 of stage[0] = word `origin`)
     const uint64_t obit = (uint64_t)origin * 32u;
-    FGC_CHECK((uint64_t)(r0 + cnt) * N - obit <= 32ull * kStageWords);
+    FGC_CHECK((uint64_t)(r0 + cnt) * N - obit <= 32ull * SelectSharedT<TH>::kStageWords);
     uint64_t lb = (uint64_t)r0 * N - obit;
 #pragma unroll
     for (int u = 0; u < 2 * kPer; ++u) {
@@ -360,13 +364,13 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
     __syncthreads();
     const uint64_t end_bit = (uint64_t)(rank_base + ttot) * N;
     const uint32_t full_end = (uint32_t)(end_bit >> 5);      // words [origin, full_end) complete
-    for (uint32_t w = origin + tid; w < full_end; w += kSelThreads) {
+    for (uint32_t w = origin + tid; w < full_end; w += TH) {
       if (w < ci.code_cap) codes[w] = sh.stage[w - origin];
       else overflow = true;
     }
     const uint32_t carry = (full_end >= origin) ? sh.stage[full_end - origin] : 0u;
     __syncthreads();
-    for (uint32_t s = tid; s < kStageWords; s += kSelThreads) sh.stage[s] = (s == 0) ? carry : 0u;
+    for (uint32_t s = tid; s < SelectSharedT<TH>::kStageWords; s += TH) sh.stage[s] = (s == 0) ? carry : 0u;
     origin = full_end;
     rank_base += ttot;
     __syncthreads();
@@ -381,9 +385,9 @@ __device__ __noinline__ void select_pack_chunk(SelectShared& sh, const ChunkInfo
   }
   // deterministic padding: bitmap pad words and the unused code capacity
   const uint32_t used = (uint32_t)(((uint64_t)rank_base * N + 31) / 32);
-  for (uint32_t w = bm_words + tid; w < (ci.code_off - kSegHeader) / 4; w += kSelThreads) bitmap[w] = 0;
+  for (uint32_t w = bm_words + tid; w < (ci.code_off - kSegHeader) / 4; w += TH) bitmap[w] = 0;
   const uint32_t cap_padded = (ci.code_cap + 3u) & ~3u;
-  for (uint32_t w = used + tid; w < cap_padded; w += kSelThreads) codes[w] = 0;
+  for (uint32_t w = used + tid; w < cap_padded; w += TH) codes[w] = 0;
   // zero the bitmap tail words beyond the last tile (none: tiles cover bins)
   if (overflow) atomicOr(flags, FGC_FLAG_CAPACITY);
 }
