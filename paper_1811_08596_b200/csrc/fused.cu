@@ -76,7 +76,7 @@ namespace {
 
 using namespace ff;
 
-constexpr int kCand = 1024;
+constexpr int kCand = 512;
 constexpr uint32_t kBins = kN + 1;                     // 32769
 constexpr uint32_t kBmWords = (2 * kBins + 31) / 32;  // 2049
 constexpr uint32_t kHalfBins = kN / 2;                 // 16384: pack split point
@@ -179,15 +179,15 @@ struct __align__(16) CompressShared {
   uint32_t hist[2048];               // pass-1 histogram of this CTA (read by the peer)
   uint32_t hist2[2048];              // pass-2 histogram of this CTA (read by the peer)
   uint32_t scan[40];
-  unsigned long long ckey[kCand];    // CTA 0: undecided bins (exact key, bin)
+  unsigned long long ckey[kCand];    // CTA 0: undecided bins (exact key, bin), pushed by both CTAs
   uint32_t cidx[kCand];
+  unsigned long long lkey[kCand];    // each CTA's own copy of CTA 0's list, sorted locally
+  uint32_t lidx[kCand];
   uint32_t ccount;                   // CTA 0: number of undecided bins
   uint32_t below;                    // per CTA: bins certainly dropped
   uint32_t anynz;                    // per CTA: any non-zero coefficient
   uint32_t rcount[2];                // per CTA: its non-zero codes landing in half 0 / half 1
   uint32_t fbin, fbelow;             // merged_bucket result
-  int mode;                          // CTA 0's decision, read by CTA 1
-  uint32_t need;
 };
 
 enum : int { kModeKeepAll = 0, kModeDropAll = 1, kModeList = 2, kModeFallback = 3 };
@@ -220,13 +220,13 @@ __device__ void merged_bucket(CompressShared& sh, const uint32_t* own, const uin
 
 // Rare paths kept out of line so the 32-way unrolled per-bin loops stay small
 // (instruction-cache pressure is the fused kernel's first-order stall).
-__device__ __noinline__ bool inband_dropped(const CompressShared* sh0, uint32_t mcount, uint32_t bin) {
+__device__ __noinline__ bool inband_dropped(const CompressShared* sh, uint32_t mcount, uint32_t bin) {
   uint32_t lo = 0, hi = mcount;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
-    if ((sh0->cidx[mid] & 0x7FFFFFFFu) < bin) lo = mid + 1; else hi = mid;
+    if ((sh->lidx[mid] & 0x7FFFFFFFu) < bin) lo = mid + 1; else hi = mid;
   }
-  return lo < mcount && (sh0->cidx[lo] & 0x7FFFFFFFu) == bin && (sh0->cidx[lo] & 0x80000000u);
+  return lo < mcount && (sh->lidx[lo] & 0x7FFFFFFFu) == bin && (sh->lidx[lo] & 0x80000000u);
 }
 
 __device__ __noinline__ void push_candidate(CompressShared* sh0, uint32_t bin, float re, float im) {
@@ -244,8 +244,8 @@ __device__ __noinline__ void resolve_candidates(CompressShared& sh, uint32_t m, 
   uint32_t M2 = 1;
   while (M2 < m) M2 <<= 1;
   for (uint32_t s = m + tid; s < M2; s += kThreads) {
-    sh.ckey[s] = ~0ull;
-    sh.cidx[s] = 0x7FFFFFFFu;
+    sh.lkey[s] = ~0ull;
+    sh.lidx[s] = 0x7FFFFFFFu;
   }
   __syncthreads();
   for (int pass = 0; pass < 2; ++pass) {
@@ -257,14 +257,14 @@ __device__ __noinline__ void resolve_candidates(CompressShared& sh, uint32_t m, 
             const bool asc = (t & k) == 0;
             bool gt;
             if (pass == 0) {
-              gt = sh.ckey[t] > sh.ckey[u] ||
-                   (sh.ckey[t] == sh.ckey[u] && (sh.cidx[t] & 0x7FFFFFFFu) > (sh.cidx[u] & 0x7FFFFFFFu));
+              gt = sh.lkey[t] > sh.lkey[u] ||
+                   (sh.lkey[t] == sh.lkey[u] && (sh.lidx[t] & 0x7FFFFFFFu) > (sh.lidx[u] & 0x7FFFFFFFu));
             } else {
-              gt = (sh.cidx[t] & 0x7FFFFFFFu) > (sh.cidx[u] & 0x7FFFFFFFu);
+              gt = (sh.lidx[t] & 0x7FFFFFFFu) > (sh.lidx[u] & 0x7FFFFFFFu);
             }
             if (gt == asc) {
-              const unsigned long long tk = sh.ckey[t]; sh.ckey[t] = sh.ckey[u]; sh.ckey[u] = tk;
-              const uint32_t ti = sh.cidx[t]; sh.cidx[t] = sh.cidx[u]; sh.cidx[u] = ti;
+              const unsigned long long tk = sh.lkey[t]; sh.lkey[t] = sh.lkey[u]; sh.lkey[u] = tk;
+              const uint32_t ti = sh.lidx[t]; sh.lidx[t] = sh.lidx[u]; sh.lidx[u] = ti;
             }
           }
         }
@@ -272,7 +272,7 @@ __device__ __noinline__ void resolve_candidates(CompressShared& sh, uint32_t m, 
       }
     }
     if (pass == 0) {
-      for (uint32_t s = tid; s < need && s < m; s += kThreads) sh.cidx[s] |= 0x80000000u;
+      for (uint32_t s = tid; s < need && s < m; s += kThreads) sh.lidx[s] |= 0x80000000u;
       __syncthreads();
     }
   }
@@ -416,7 +416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   }
 
   FGC_TS(3);
-  // ---- 4. count-mode selection, cluster-wide (cluster barriers A-D)
+  // ---- 4. count-mode selection, cluster-wide (cluster barriers A-C)
   const uint32_t kdrop = ci.drop;
   int mode = kModeList;
   if (kdrop == 0) mode = kModeKeepAll;
@@ -507,22 +507,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     }
     FGC_TS(9);
     cluster.sync();                               // C: candidates and counts visible
-    if (r == 0) {
-      if (tid == 0) {
-        int md = mode;
-        const uint32_t m = sh.ccount;
-        const uint32_t below = sh.below + shp.below;
-        if (md == kModeList && (m > (uint32_t)kCand || below > kdrop || below + m < kdrop)) md = kModeFallback;
-        sh.need = kdrop - below;
-        sh.mode = md;
+    // Both CTAs copy CTA 0's candidate list and resolve it themselves: the
+    // same data and order give the same decision, and no barrier waits for a
+    // single resolving CTA.
+    {
+      const uint32_t m = sh0.ccount;
+      const uint32_t below = sh.below + shp.below;
+      if (mode == kModeList && (m > (uint32_t)kCand || below > kdrop || below + m < kdrop)) mode = kModeFallback;
+      if (mode == kModeList) {
+        for (uint32_t s = tid; s < m; s += kThreads) {
+          sh.lkey[s] = sh0.ckey[s];
+          sh.lidx[s] = sh0.cidx[s];
+        }
+        __syncthreads();
+        resolve_candidates(sh, m, kdrop - below);
+        mcount = m;
       }
-      __syncthreads();
-      if (sh.mode == kModeList) resolve_candidates(sh, sh.ccount, sh.need);
     }
     FGC_TS(10);
-    cluster.sync();                               // D: decisions visible
-    mode = sh0.mode;
-    mcount = (mode == kModeList) ? sh0.ccount : 0u;
   } else {
     cluster.sync();                               // D': both bitmaps zeroed (peer atomics follow)
   }
@@ -537,7 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     }
     if (special) out[kN] = xn;
     __threadfence();
-    cluster.sync();          // both halves written; the peer finished reading sh0.mode
+    cluster.sync();          // both halves written; both CTAs finished reading CTA 0's list
     if (r == 1) return;
     // CTA 0 selects and packs the chunk with the generic single-CTA code,
     // its scratch in the (now free) transpose buffer
@@ -570,7 +572,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     constexpr uint32_t d = decltype(D)::value;
     const float p = proxy_key(x.x, x.y);
     bool keep = p >= lo_b;
-    if (keep && p < hi_b) keep = !inband_dropped(&sh0, mcount, bin);
+    if (keep && p < hi_b) keep = !inband_dropped(&sh, mcount, bin);
     if (keep) {
       const uint32_t cre = enc16(q, x.x), cim = enc16(q, x.y);
       const uint32_t pc = cre | (cim << 16);
@@ -601,7 +603,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     const uint32_t b = __ffs(band) - 1u;
     band &= band - 1u;
     const uint32_t bin = 2u * (((b & 1u) ? kb : ka) + 1024u * (b >> 1)) + r;
-    if (!inband_dropped(&sh0, mcount, bin)) keep |= 1u << b;
+    if (!inband_dropped(&sh, mcount, bin)) keep |= 1u << b;
   }
   // Only ~1 value in 10 is kept, so encoding every value in every lane would
   // spend most of the phase on dropped bins.  Per round of 4 j (8 values per
