@@ -249,6 +249,14 @@ fgc_status fgc_bitmap_to_flags(const uint8_t* bitmap, uint64_t count, uint8_t* f
  * ceil(count/4096)+1 entries. */
 fgc_status fgc_prefix_sum(const uint8_t* status01, uint64_t count, int64_t* out, uint32_t* bad,
                           uint64_t* scratch, void* stream);
+/* pack's scatter (packer.py:55-57): dense[loc[i] - 1] = values[i] where
+ * status01[i], loc = the inclusive prefix_sum above; elem_bytes 1/2/4/8. */
+fgc_status fgc_compact(const void* values, const uint8_t* status01, const int64_t* loc, uint64_t count,
+                       int elem_bytes, void* dense, void* stream);
+/* unpack's gather (packer.py:67-69): out[i] = status01[i] ? dense[loc[i] - 1]
+ * : 0. */
+fgc_status fgc_expand(const void* dense, const uint8_t* status01, const int64_t* loc, uint64_t count,
+                      int elem_bytes, void* out, void* stream);
 
 /* dft_forward / dft_inverse of ONE length-L real signal (spectral.py:88-106)
  * in float64 like the reference: any L >= 1, float32/float64 input,

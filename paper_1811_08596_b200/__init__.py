@@ -19,5 +19,7 @@ from .packer import PackedSparse, pack, unpack, prefix_sum, bitmap_to_bytes, bit
 from .codec import (CodecConfig, ChunkPayload, CompressedMessage, compress, decompress, reconstruct,
                     reconstruct_rows, serialize, deserialize, calibrate, compression_ratio)
 from .comm import GradientAverager, NcclComm, PeerExchange, allgather_average, message_layout, shard_weights
+from .simulator import (QuadraticProblem, LogisticProblem, MlpProblem, make_problem, LrSchedule, ThetaSchedule,
+                        TrainConfig, ConvergenceTrace, sub_gradient, step, run, gradient_stats)
 
 __version__ = "0.1.0"

@@ -82,6 +82,8 @@ _SIGS = {
     "fgc_flags_to_bitmap": (I32, [P, U64, P, P]),
     "fgc_bitmap_to_flags": (I32, [P, U64, P, P]),
     "fgc_prefix_sum": (I32, [P, U64, P, P, P, P]),
+    "fgc_compact": (I32, [P, P, P, U64, I32, P, P]),
+    "fgc_expand": (I32, [P, P, P, U64, I32, P, P]),
     "fgc_rfft": (I32, [P, I32, U64, P, P, P]),
     "fgc_irfft": (I32, [P, U64, P, P]),
     "fgc_truncate": (I32, [P, U64, F64, P, P, P]),

@@ -205,9 +205,10 @@ class GradientAverager:
 
     def _check_out(self, out: torch.Tensor) -> torch.Tensor:
         if (not isinstance(out, torch.Tensor) or not out.is_cuda or out.device != self.out.device
-                or out.dtype != torch.float32 or out.numel() != self.n or not out.is_contiguous()):
-            raise ValueError("out must be a contiguous float32 CUDA tensor of the planned length "
-                             "on the averager's device")
+                or out.dtype != torch.float32 or out.numel() != self.n or not out.is_contiguous()
+                or out.data_ptr() % 8):
+            raise ValueError("out must be a contiguous, 8-byte aligned float32 CUDA tensor of the planned "
+                             "length on the averager's device")
         return out
 
     def step(self, grad: torch.Tensor, out: torch.Tensor | None = None, theta: float | None = None) -> torch.Tensor:

@@ -46,6 +46,24 @@ static fgc_status check_signal(const void* g, int dtype) {
   return FGC_OK;
 }
 
+// The decode kernels load message segments 16 bytes at a time.
+static fgc_status check_messages(const uint8_t* m, uint64_t stride) {
+  if (reinterpret_cast<uintptr_t>(m) % 16 || stride % 16) {
+    set_error("device messages must be 16-byte aligned with a 16-byte multiple stride");
+    return FGC_ERR_INVALID;
+  }
+  return FGC_OK;
+}
+
+// The decode kernels store two output samples at a time (float2).
+static fgc_status check_out(const float* out) {
+  if (reinterpret_cast<uintptr_t>(out) % 8) {
+    set_error("float32 output must be 8-byte aligned");
+    return FGC_ERR_INVALID;
+  }
+  return FGC_OK;
+}
+
 }  // namespace fgc
 
 using namespace fgc;
@@ -492,6 +510,8 @@ static fgc_status decode_range(fgc_plan* p, const uint8_t* messages, int W, uint
 extern "C" fgc_status fgc_decode_average(fgc_plan* p, const uint8_t* messages, int W, uint64_t stride,
                                          const double* weights, float* out, void* stream) {
   if (!p || !messages || !out) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_out(out));
+  FGC_TRY(check_messages(messages, stride));
   Weights w;
   FGC_TRY(fill_weights(weights, W, w));
   return decode_range(p, messages, W, stride, w, out, static_cast<cudaStream_t>(stream), p->fused_first,
@@ -501,6 +521,7 @@ extern "C" fgc_status fgc_decode_average(fgc_plan* p, const uint8_t* messages, i
 extern "C" fgc_status fgc_decode_spectrum(fgc_plan* p, const uint8_t* messages, int W, uint64_t stride,
                                           const double* weights, void* spectrum, void* stream) {
   if (!p || !messages || !spectrum) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_messages(messages, stride));
   Weights w;
   FGC_TRY(fill_weights(weights, W, w));
   return launch_decode_accumulate(p->d_chunks, 0, p->n_chunks, messages, W, stride, w, p->q,
@@ -509,6 +530,7 @@ extern "C" fgc_status fgc_decode_spectrum(fgc_plan* p, const uint8_t* messages, 
 
 extern "C" fgc_status fgc_inverse_spectrum(fgc_plan* p, const void* spectrum, float* out, void* stream) {
   if (!p || !spectrum || !out) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_out(out));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (RealClass& rc : p->classes) {
     if (!rc.fused) continue;
@@ -671,6 +693,7 @@ extern "C" fgc_status fgc_allgather_average(fgc_plan* p, void* comm, int nranks,
                                             const double* weights, uint8_t* message, uint8_t* gathered, float* out,
                                             uint32_t* flags, void* stream) {
   if (!p || !grad || !message || !out || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_out(out));
   if (nranks <= 1) {
     if (!p->fused_count || p->desc.mode != FGC_MODE_COUNT || !overlap_enabled()) {
       FGC_TRY(fgc_compress(p, grad, dtype, message, flags, stream));
@@ -804,6 +827,7 @@ static fgc_status exchange_average_impl(fgc_plan* p, fgc_exchange* x, const void
                                         const double* weights, float* out, uint32_t* flags, void* stream,
                                         bool* started) {
   if (!p || !x || !grad || !out || !flags) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_out(out));
   if (!exchange_ready(x)) return exchange_not_ready(x);
   FGC_TRY(check_mode(p));
   FGC_TRY(check_signal(grad, dtype));
@@ -926,6 +950,7 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
   }
   FGC_TRY(check_mode(p));
   FGC_TRY(check_signal(dev_grad, dtype));
+  FGC_TRY(check_out(dev_out));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int W = 1, me = 0;
   uint32_t* counter = nullptr;

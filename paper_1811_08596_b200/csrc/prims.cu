@@ -16,6 +16,8 @@
 
 #include <vector>
 
+#include <algorithm>
+
 #include "fgc_device.cuh"
 #include "fgc_internal.h"
 
@@ -256,6 +258,59 @@ extern "C" fgc_status fgc_prefix_sum(const uint8_t* status01, uint64_t count, in
   k_tile_apply<<<(uint32_t)tiles, kScanThreads, 0, s>>>(status01, count, scratch, reinterpret_cast<long long*>(out));
   FGC_LAUNCHED(1);
   return FGC_OK;
+}
+
+template <class E>
+__global__ void k_compact(const E* v, const uint8_t* st, const long long* loc, uint64_t n, E* dense) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (st[i]) dense[loc[i] - 1] = v[i];
+}
+template <class E>
+__global__ void k_expand(const E* dense, const uint8_t* st, const long long* loc, uint64_t n, E* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = st[i] ? dense[loc[i] - 1] : E(0);
+}
+
+template <template <class> class K, class... A>
+static fgc_status launch_by_size(int elem_bytes, uint64_t n, cudaStream_t s, const void* a, const uint8_t* st,
+                                 const int64_t* loc, void* b) {
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+  const long long* l = reinterpret_cast<const long long*>(loc);
+  switch (elem_bytes) {
+    case 1: K<uint8_t>::run(grid, s, a, st, l, n, b); break;
+    case 2: K<uint16_t>::run(grid, s, a, st, l, n, b); break;
+    case 4: K<uint32_t>::run(grid, s, a, st, l, n, b); break;
+    case 8: K<unsigned long long>::run(grid, s, a, st, l, n, b); break;
+    default: set_error("elem_bytes must be 1, 2, 4 or 8"); return FGC_ERR_INVALID;
+  }
+  FGC_LAUNCHED(1);
+  return FGC_OK;
+}
+template <class E> struct CompactK {
+  static void run(uint32_t g, cudaStream_t s, const void* a, const uint8_t* st, const long long* l, uint64_t n,
+                  void* b) {
+    k_compact<E><<<g, 256, 0, s>>>(static_cast<const E*>(a), st, l, n, static_cast<E*>(b));
+  }
+};
+template <class E> struct ExpandK {
+  static void run(uint32_t g, cudaStream_t s, const void* a, const uint8_t* st, const long long* l, uint64_t n,
+                  void* b) {
+    k_expand<E><<<g, 256, 0, s>>>(static_cast<const E*>(a), st, l, n, static_cast<E*>(b));
+  }
+};
+
+extern "C" fgc_status fgc_compact(const void* values, const uint8_t* status01, const int64_t* loc, uint64_t count,
+                                  int elem_bytes, void* dense, void* stream) {
+  if (!count) return FGC_OK;
+  if (!values || !status01 || !loc || !dense) { set_error("null argument"); return FGC_ERR_INVALID; }
+  return launch_by_size<CompactK>(elem_bytes, count, static_cast<cudaStream_t>(stream), values, status01, loc, dense);
+}
+
+extern "C" fgc_status fgc_expand(const void* dense, const uint8_t* status01, const int64_t* loc, uint64_t count,
+                                 int elem_bytes, void* out, void* stream) {
+  if (!count) return FGC_OK;
+  if (!dense || !status01 || !loc || !out) { set_error("null argument"); return FGC_ERR_INVALID; }
+  return launch_by_size<ExpandK>(elem_bytes, count, static_cast<cudaStream_t>(stream), dense, status01, loc, out);
 }
 
 extern "C" fgc_status fgc_rfft(const void* signal, int dtype, uint64_t L, void* spectrum, uint32_t* flags,

@@ -1,8 +1,8 @@
 """Stream compaction -- drop-in for ``fgc.packer`` (pkg/src/fgc/packer.py).
 
-``prefix_sum`` and the bitmap byte conversions run as CUDA kernels; ``pack``
-/ ``unpack`` compact with a device scan + scatter (torch index ops on the
-device for the value gather, the scan itself is ours)."""
+``prefix_sum``, the bitmap byte conversions and ``pack`` / ``unpack`` (a
+device scan, then the scatter / gather kernels fgc_compact / fgc_expand) run
+as this package's CUDA kernels."""
 
 from __future__ import annotations
 
@@ -58,26 +58,30 @@ def prefix_sum(status) -> np.ndarray:
     return _device_scan(t).cpu().numpy()
 
 
+def _elem(values: np.ndarray) -> tuple:
+    """(contiguous array, element bytes) for the device copy."""
+    v = np.ascontiguousarray(values)
+    if v.dtype.itemsize not in (1, 2, 4, 8):
+        raise ValueError(f"unsupported element size {v.dtype.itemsize}")
+    return v, v.dtype.itemsize
+
+
 def pack(sparse) -> PackedSparse:
     """packer.py:49-58: status -> scan -> scatter to dense[loc-1]."""
     values = np.asarray(sparse)
     if values.size == 0:
         return PackedSparse(np.zeros(0, dtype=bool), np.empty(0, dtype=values.dtype), 0)
     dev = D.require_cuda()
-    flat = values.reshape(-1)
-    status = torch.from_numpy(np.ascontiguousarray(flat != 0).astype(np.uint8)).to(dev)
+    flat, eb = _elem(values.reshape(-1))
+    status = torch.from_numpy((flat != 0).astype(np.uint8)).to(dev)
     loc = _device_scan(status)
     kept = int(loc[-1].item())
-    marked = status.bool()
-    vals = torch.from_numpy(np.ascontiguousarray(flat)).to(dev) if flat.dtype != np.uint32 else \
-        torch.from_numpy(flat.view(np.int32).copy()).to(dev)
-    dense = torch.empty(kept, dtype=vals.dtype, device=dev)
-    dense[loc[marked] - 1] = vals[marked]
-    d = dense.cpu().numpy()
-    if flat.dtype == np.uint32:
-        d = d.view(np.uint32)
-    return PackedSparse(bitmap=marked.cpu().numpy(), dense=d.astype(values.dtype, copy=False),
-                        original_len=values.size)
+    src = torch.from_numpy(flat.view(np.uint8)).to(dev)
+    dense = torch.empty(max(1, kept * eb), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.lib.fgc_compact(src.data_ptr(), status.data_ptr(), loc.data_ptr(), flat.size, eb,
+                                    dense.data_ptr(), D.stream()))
+    d = dense[:kept * eb].cpu().numpy().view(flat.dtype)
+    return PackedSparse(bitmap=status.cpu().numpy().astype(bool), dense=d, original_len=values.size)
 
 
 def unpack(packed: PackedSparse) -> np.ndarray:
@@ -88,14 +92,14 @@ def unpack(packed: PackedSparse) -> np.ndarray:
     out = np.zeros(packed.original_len, dtype=packed.dense.dtype)
     if kept:
         dev = D.require_cuda()
-        mask = torch.from_numpy(np.ascontiguousarray(packed.bitmap)).to(dev)
-        dense = packed.dense
-        is_u32 = dense.dtype == np.uint32
-        src = torch.from_numpy(dense.view(np.int32).copy() if is_u32 else np.ascontiguousarray(dense)).to(dev)
-        full = torch.zeros(packed.original_len, dtype=src.dtype, device=dev)
-        full[mask] = src
-        r = full.cpu().numpy()
-        out = r.view(np.uint32) if is_u32 else r
+        dense, eb = _elem(packed.dense)
+        status = torch.from_numpy(np.ascontiguousarray(packed.bitmap).astype(np.uint8)).to(dev)
+        loc = _device_scan(status)
+        src = torch.from_numpy(dense.view(np.uint8)).to(dev)
+        full = torch.empty(packed.original_len * eb, dtype=torch.uint8, device=dev)
+        _lib.check(_lib.lib.fgc_expand(src.data_ptr(), status.data_ptr(), loc.data_ptr(), packed.original_len, eb,
+                                       full.data_ptr(), D.stream()))
+        out = full.cpu().numpy().view(dense.dtype).copy()
     return out
 
 

@@ -862,3 +862,33 @@ def test_runtime_theta_one_plan():
     with pytest.raises(ValueError):
         avg.step(g, out=torch.empty(n - 1, device="cuda"))
     avg.close()
+
+
+@pytest.mark.parametrize("n,chunk,theta,mode", [(3000, 512, 0.9, "count"), (70_001, 65536, 0.7, "count"),
+                                                (5000, 1024, 0.5, "energy")])
+def test_reconstruct_rows_matches_rows(n, chunk, theta, mode):
+    """codec.py:292-337: the batched rows call equals reconstruct() row by
+    row bit for bit (test_codec.py:138-152 asserts the same of the
+    reference), and the oracle within the decode tolerance."""
+    rng = np.random.default_rng(n)
+    rows = rng.standard_normal((3, n)) * 1e-2
+    q = F.calibrate([rows[0]], 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta, mode), q, chunk_size=chunk)
+    got = F.reconstruct_rows(rows, cfg)
+    assert got.shape == rows.shape and got.dtype == np.float64
+    for i in range(rows.shape[0]):
+        np.testing.assert_array_equal(got[i], F.reconstruct(rows[i], cfg))
+    ref = O.reconstruct_rows(rows, theta, mode, lat_of(q), False, chunk)
+    assert rel_l2(got, ref) <= 1e-5
+
+
+def test_pack_unpack_dtypes():
+    """packer.py:49-70 through the device scatter / gather kernels."""
+    rng = np.random.default_rng(5)
+    for dt in (np.float64, np.float32, np.uint32, np.int16, np.uint8):
+        v = (rng.integers(0, 3, 10_001) * rng.integers(1, 100, 10_001)).astype(dt)
+        p = F.pack(v)
+        np.testing.assert_array_equal(p.bitmap, v != 0)
+        np.testing.assert_array_equal(p.dense, v[v != 0])
+        assert p.dense.dtype == v.dtype
+        np.testing.assert_array_equal(F.unpack(p), v)
