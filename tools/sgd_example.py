@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--cap", type=float, default=0.99)
     ap.add_argument("--nbits", type=int, default=8)
     ap.add_argument("--mantissa", type=int, default=3)
+    ap.add_argument("--passthrough", action="store_true", help="no quantizer (raw float32 codes)")
     a = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -76,7 +77,7 @@ def main():
         eta = eta0 / (1.0 + t / a.tau) ** a.power
         theta = min(a.cap, math.sqrt(L * eta))
         g = A.T @ (A @ x - b) / a.rows
-        if q is None:                                   # range fixed from the first gradient (simulator.py:354)
+        if q is None and not a.passthrough:            # range fixed from the first gradient (simulator.py:354)
             q = F.calibrate([g], a.nbits, a.mantissa)
         if avg is None:
             avg = GradientAverager(a.dim, F.CodecConfig(F.SparsificationSpec(theta), q), w, comm,
