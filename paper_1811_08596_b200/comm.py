@@ -27,7 +27,8 @@ from . import _device as D
 from . import _lib
 from .codec import CodecConfig, Plan, _desc
 
-__all__ = ["message_layout", "shard_weights", "NcclComm", "PeerExchange", "GradientAverager", "allgather_average"]
+__all__ = ["message_layout", "shard_weights", "config_fingerprint", "check_config_agreement", "NcclComm",
+           "PeerExchange", "GradientAverager", "allgather_average"]
 
 
 def message_layout(n: int, config: CodecConfig) -> tuple[int, int, np.ndarray]:
@@ -48,6 +49,34 @@ def shard_weights(batch_size: int, workers: int) -> np.ndarray:
     np.array_split of the batch; weight = shard_size / batch_size."""
     sizes = np.array([len(p) for p in np.array_split(np.arange(batch_size), workers)])
     return sizes / batch_size
+
+
+def config_fingerprint(n: int, config: CodecConfig, capacity_theta: float | None, weights) -> tuple:
+    """What every rank of one averaging group must agree on: length, chunk,
+    capacity theta (the message layout), mode, half pass, quantizer lattice
+    and the shard weights."""
+    q = config.quantizer
+    spec = config.sparsification
+    cap = spec.theta if capacity_theta is None else float(capacity_theta)
+    return (int(n), int(config.chunk_size), cap, spec.mode, bool(config.half_precision_pass),
+            None if q is None else (q.min, q.max, q.n_bits, q.mantissa_bits, q.eps),
+            tuple(float(x) for x in np.asarray(weights, dtype=np.float64).reshape(-1)))
+
+
+def check_config_agreement(fingerprint: tuple, group=None, world: int | None = None) -> None:
+    """Every rank decodes every other rank's codes with its own plan and
+    lattice: a rank with another quantizer, length or capacity would average
+    garbage silently.  Compare fingerprints once, on all ranks (any
+    torch.distributed backend); every rank raises the same ValueError."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if world is None else world
+    allf = [None] * world
+    dist.all_gather_object(allf, fingerprint, group=group)
+    bad = [r for r, f in enumerate(allf) if f != allf[0]]
+    if bad:
+        raise ValueError(f"ranks {bad} disagree with rank 0 on the codec configuration (length, chunk, capacity "
+                         f"theta, mode, quantizer, weights): every rank must average with the same config, e.g. a "
+                         f"quantizer calibrated once and broadcast")
 
 
 class NcclComm:
@@ -179,6 +208,8 @@ class GradientAverager:
         self.out = torch.empty(self.n, dtype=torch.float32, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
         import os
+        if self.world > 1:
+            self._check_agreement(comm)
         self.transport = transport or os.environ.get("FGC_TRANSPORT", "peer")
         if self.transport not in ("peer", "nccl"):
             raise ValueError(f"unknown transport {self.transport!r}")
@@ -190,6 +221,10 @@ class GradientAverager:
                 import warnings
                 warnings.warn(f"{e}; using the NCCL allgather")
                 self.transport = "nccl"
+
+    def _check_agreement(self, comm) -> None:
+        check_config_agreement(config_fingerprint(self.n, self.config, self.capacity_theta, self.weights),
+                               comm.group, self.world)
 
     def close(self) -> None:
         if self.exchange is not None:

@@ -231,6 +231,7 @@ __device__ __noinline__ bool inband_dropped(const CompressShared* sh, uint32_t m
 
 __device__ __noinline__ void push_candidate(CompressShared* sh0, uint32_t bin, float re, float im) {
   const uint32_t s = atomicAdd(&sh0->ccount, 1u);
+  FGC_CHECK(bin <= kN);
   if (s < (uint32_t)kCand) {
     sh0->cidx[s] = bin;
     sh0->ckey[s] = (unsigned long long)__double_as_longlong(cabs_key((double)re, (double)im));
@@ -580,6 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         const uint32_t c = (cre ? 1u : 0u) + (cim ? 1u : 0u);
         if (d) rc1 += c; else rc0 += c;
         const uint32_t lb = bin - d * kHalfBins;
+        FGC_CHECK(lb <= kHalfBins && pad(lb) < kStageOff);
         const uint32_t bits = ((cre ? 1u : 0u) | (cim ? 2u : 0u)) << (2u * (lb & 15u));
         if (d == r) {
           arr_own[pad(lb)] = pc;
@@ -631,6 +633,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         constexpr int k = decltype(K)::value;
         constexpr int j = j0 + k / 2;
         if ((m8 >> k) & 1u) {
+          FGC_CHECK(pos < 256u);
           wmeta[pos] = (k & 1) ? BIN_B(j) : BIN_A(j);
           wval[pos] = (k & 1) ? vb[j] : va[j];
           ++pos;
@@ -646,6 +649,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           const uint32_t c = (cre ? 1u : 0u) + (cim ? 1u : 0u);
           if (d) rc1 += c; else rc0 += c;
           const uint32_t lb = bin - d * kHalfBins;
+          FGC_CHECK(lb <= kHalfBins && pad(lb) < kStageOff);
           const uint32_t bits = ((cre ? 1u : 0u) | (cim ? 2u : 0u)) << (2u * (lb & 15u));
           if (d == r) {
             arr_own[pad(lb)] = pc;
@@ -707,6 +711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   const uint32_t wstart = (uint32_t)(S >> 5), o = (uint32_t)(S & 31u);
   const uint32_t nwords = (uint32_t)((o + (uint64_t)total * N + 31) / 32);
   uint32_t* stg = arr_own + kStageOff;
+  FGC_CHECK(kStageOff + nwords + 1 <= 2 * (kPadded + 64));
   for (uint32_t k = tid; k < nwords; k += kThreads) stg[k] = 0u;
   __syncthreads();
   {
@@ -720,6 +725,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         m64 &= m64 - 1;
         const uint32_t pc = src[pos >> 1];
         const uint32_t code = (pos & 1) ? (pc >> 16) : (pc & 0xFFFFu);
+        FGC_CHECK((lbit >> 5) < nwords);
         if (N == 8) {
           stg8[lbit >> 3] = (uint8_t)code;                // byte-aligned codes: plain stores
         } else {
@@ -953,6 +959,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             const uint8_t* sg = a.messages + (uint64_t)(w0 + i) * a.stride + ci.seg_off;
             const uint32_t nnz = __ldg(reinterpret_cast<const uint32_t*>(sg));
             const uint32_t used4 = (uint32_t)min((((uint64_t)nnz * N + 127u) >> 7), (uint64_t)((ci.code_cap + 3u) >> 2));
+            FGC_CHECK(nnz <= 2u * ci.bins);
             if (!(dbg & 4u) && used_total + 4u * used4 <= kDecStageWords) {
               soff[i] = used_total;
               if (tid == 0) sh.soff[i] = used_total;
@@ -1021,6 +1028,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
               while (m) {
                 const uint32_t pos = __ffs(m) - 1;
                 m &= m - 1;
+                FGC_CHECK(k < 4u * (kDecStageWords - so));
                 add(f, pos, s8[k++], wt);
               }
             };
@@ -1033,6 +1041,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
               while (m) {
                 const uint32_t pos = __ffs(m) - 1;
                 m &= m - 1;
+                FGC_CHECK(k < 2u * (kDecStageWords - so));
                 add(f, pos, s16[k++], wt);
               }
             };
@@ -1047,6 +1056,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
                 const uint32_t pos = __ffs(m) - 1;
                 m &= m - 1;
                 const uint32_t wi = bit >> 5;
+                FGC_CHECK(so + wi + 1 < kDecStageWords + 8);
                 add(f, pos, __funnelshift_r(st[wi], st[wi + 1], bit & 31u) & mask, wt);
                 bit += N;
               }

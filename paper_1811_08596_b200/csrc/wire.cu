@@ -79,6 +79,7 @@ __global__ void k_wire_copy(const ChunkInfo* chunks, const uint8_t* message, int
   const uint32_t nnz = *reinterpret_cast<const uint32_t*>(seg);
   const uint64_t bmb = (ci.slots + 7) / 8;
   const uint64_t cb = ((uint64_t)nnz * N + 7) / 8;
+  FGC_CHECK(nnz <= ci.slots && (uint64_t)nnz * N <= 32ull * ci.code_cap);
   uint8_t* dst = wire + FGC_HEADER_BYTES + offsets[c];
   const uint64_t total = 4 + bmb + cb;
   for (uint64_t j = threadIdx.x; j < total; j += blockDim.x) {
@@ -151,6 +152,7 @@ __global__ void k_message_unpack(const ChunkInfo* chunks, const uint8_t* message
   const uint32_t* bm = reinterpret_cast<const uint32_t*>(seg + kSegHeader);
   const uint32_t* cw = reinterpret_cast<const uint32_t*>(seg + ci.code_off);
   const uint32_t nnz = *reinterpret_cast<const uint32_t*>(seg);
+  FGC_CHECK(nnz <= ci.slots && (uint64_t)nnz * N <= 32ull * ci.code_cap);
   for (uint32_t s = threadIdx.x; s < ci.slots; s += blockDim.x) {
     const uint32_t so = ballot_to_wire(bm[s >> 5]);
     flags01[ci.slot_off + s] = (so >> (s & 31)) & 1u;

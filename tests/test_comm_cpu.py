@@ -84,3 +84,41 @@ def test_two_rank_exchange_and_average(theta, nm):
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     results = dict(q.get(timeout=10) for _ in range(WORLD))
     assert all(err <= 1e-12 for err in results.values()), results
+
+
+def _agree_worker(rank, port, differ, out_q):
+    from paper_1811_08596_b200.comm import check_config_agreement, config_fingerprint
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        # a quantizer calibrated per rank instead of once: rank 1's lattice differs
+        q = F.tune_eps(-0.5, 0.5 if (rank == 0 or not differ) else 0.7, 8, 3)
+        cfg = F.CodecConfig(F.SparsificationSpec(0.9), q, chunk_size=CHUNK)
+        try:
+            check_config_agreement(config_fingerprint(N, cfg, None, shard_weights(8, WORLD)))
+            out_q.put((rank, "ok"))
+        except ValueError as e:
+            out_q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("differ", [False, True])
+def test_config_agreement_across_ranks(differ):
+    """GradientAverager refuses to average when the ranks' codec configs differ
+    (every rank decodes the others' codes with its own lattice)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, port, differ, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    res = dict(q.get(timeout=10) for _ in range(WORLD))
+    if differ:
+        assert all("disagree" in v for v in res.values()), res
+    else:
+        assert all(v == "ok" for v in res.values()), res

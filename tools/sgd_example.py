@@ -77,8 +77,14 @@ def main():
         eta = eta0 / (1.0 + t / a.tau) ** a.power
         theta = min(a.cap, math.sqrt(L * eta))
         g = A.T @ (A @ x - b) / a.rows
-        if q is None and not a.passthrough:            # range fixed from the first gradient (simulator.py:354)
-            q = F.calibrate([g], a.nbits, a.mantissa)
+        if q is None and not a.passthrough:
+            # one range for every rank, fixed from rank 0's first gradient
+            # (TrainConfig.quantizer, simulator.py:354): ranks decode each
+            # other's codes with it
+            g0 = g.clone()
+            if world > 1:
+                torch.distributed.broadcast(g0, src=0)
+            q = F.calibrate([g0], a.nbits, a.mantissa)
         if avg is None:
             avg = GradientAverager(a.dim, F.CodecConfig(F.SparsificationSpec(theta), q), w, comm,
                                    capacity_theta=0.0)
