@@ -1035,17 +1035,25 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
   // half-size first and last pieces: shorter pipeline fill (first copy-in)
   // and drain (last copy-out)
   const bool ramp = P >= 3 && p->fused_count >= 2 * P && !getenv("FGC_HOST_NO_RAMP");
+  // ramp: first piece 1/2, last piece 1/tq of the middle pieces (in units of 1/tq)
+  uint64_t tq = 8;                                     // measured: 2.615 ms (8) vs 2.62-2.66 (2, 4) at 25.6M
+  if (const char* e = getenv("FGC_HOST_TAIL")) tq = (uint64_t)std::max(2, atoi(e));
   for (uint32_t i = 0; i <= P; ++i) {
-    const uint64_t u = ramp ? (i == 0 ? 0 : i == P ? 2 * P - 2 : 2 * i - 1) : i;     // in half-pieces
-    const uint64_t un = ramp ? 2 * P - 2 : (P ? P : 1);
+    uint64_t u = i, un = P ? P : 1;
+    if (ramp) {
+      un = tq / 2 + tq * (P - 2) + 1;
+      u = i == 0 ? 0 : i == P ? un : tq / 2 + tq * (i - 1);
+    }
     f[i] = p->fused_first + (uint32_t)((uint64_t)p->fused_count * u / un);
   }
   auto elem_lo = [&](uint32_t i) -> uint64_t { return p->chunks[f[i]].in_off; };
   auto elem_hi = [&](uint32_t i) -> uint64_t { return i + 1 == P ? g_lo : p->chunks[f[i + 1]].in_off; };
   auto seg_hi = [&](uint32_t i) -> uint64_t { return i + 1 == P ? m_lo : p->seg_off[f[i + 1]]; };
+  exchange_trace(p->h2d, "start");
   for (uint32_t i = 0; i < P; ++i) {
     FGC_CUDA(h2d(elem_lo(i), elem_hi(i)));
     FGC_CUDA(cudaEventRecord(p->ev_h[i], p->h2d));
+    exchange_trace(p->h2d, "h2d");
   }
   for (uint32_t i = 0; i < P; ++i) {
     FGC_CUDA(cudaStreamWaitEvent(s, p->ev_h[i], 0));
@@ -1058,6 +1066,7 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
       // W = 1: decode this piece right away so its copy-out overlaps the next pieces
       FGC_TRY(decode_range(p, message, 1, p->msg_bytes, w, dev_out, s, f[i], f[i + 1] - f[i], false));
       FGC_CUDA(cudaEventRecord(p->ev_d[i], s));
+      exchange_trace(s, "dec");
     }
   }
   if (x) {
@@ -1071,10 +1080,12 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
   if (generic) {
     FGC_CUDA(cudaStreamWaitEvent(p->d2h, p->ev_d[P], 0));
     FGC_CUDA(d2h(g_lo, p->desc.n));
+    exchange_trace(p->d2h, "d2h-tail");
   }
   for (uint32_t i = 0; i < P; ++i) {
     FGC_CUDA(cudaStreamWaitEvent(p->d2h, p->ev_d[i], 0));
     FGC_CUDA(d2h(elem_lo(i), elem_hi(i)));
+    exchange_trace(p->d2h, "d2h");
   }
   FGC_CUDA(cudaEventRecord(p->ev_step, p->d2h));
   FGC_CUDA(cudaStreamWaitEvent(s, p->ev_step, 0));
