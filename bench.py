@@ -109,10 +109,10 @@ class ClockSampler:
 # ---------------------------------------------------------------- reference arm
 
 def _ref_chunk_job(args):
-    g_bytes, theta, lat, chunk = args
+    g_bytes, theta, lat, chunk, mode = args
     import oracle as O
     g = np.frombuffer(g_bytes, dtype=np.float32).astype(np.float64)
-    msg = O.compress(g, theta, "count", lat, False, chunk)
+    msg = O.compress(g, theta, mode, lat, False, chunk)
     wire = O.to_wire(msg)
     return O.decompress(O.from_wire(wire))
 
@@ -130,12 +130,13 @@ def cpu_reference(wl: dict, seconds_budget: float, cores: int | None = None, sam
     probe = (rng.standard_normal(chunk) * 1e-2).astype(np.float32)
     lat = O.calibrate([probe], wl["n_bits"], wl["mbits"])
     t0 = time.perf_counter()
-    _ref_chunk_job((probe.tobytes(), wl["theta"], lat, chunk))
+    mode = wl.get("mode", "count")
+    _ref_chunk_job((probe.tobytes(), wl["theta"], lat, chunk, mode))
     per_chunk = time.perf_counter() - t0
     if sample_chunks is None:
         sample_chunks = int(max(cores, min(wl["n"] // chunk, seconds_budget * cores / max(per_chunk, 1e-3))))
     g = (rng.standard_normal(sample_chunks * chunk) * 1e-2).astype(np.float32)
-    jobs = [(g[i * chunk:(i + 1) * chunk].tobytes(), wl["theta"], lat, chunk) for i in range(sample_chunks)]
+    jobs = [(g[i * chunk:(i + 1) * chunk].tobytes(), wl["theta"], lat, chunk, mode) for i in range(sample_chunks)]
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
         t0 = time.perf_counter()
@@ -202,9 +203,12 @@ def run_reference(args, wl, rank, world):
 
 
 def workload_config(args, wl, world):
-    return {"workload": f"{args.workload}: n={wl['n']} floats, keep={1 - wl['theta']:.2f} "
-                        f"(reference theta_drop={wl['theta']}), {wl['n_bits']}-bit range float m={wl['mbits']}, "
-                        f"chunk={wl['chunk']}, W={world} ranks",
+    mode = wl.get("mode", "count")
+    keep = (f"keep={1 - wl['theta']:.2f} (reference theta_drop={wl['theta']})" if mode == "count" else
+            f"energy mode, theta={wl['theta']} (drop while cumulative energy <= theta^2 of the total)")
+    return {"workload": f"{args.workload}: n={wl['n']} floats, {keep}, {wl['n_bits']}-bit range float "
+                        f"m={wl['mbits']}, chunk={wl['chunk']}, W={world} ranks",
+            "mode": mode,
             "n": wl["n"], "theta_drop": wl["theta"], "n_bits": wl["n_bits"], "mantissa_bits": wl["mbits"],
             "chunk_size": wl["chunk"], "world": world, "parallelism": f"dp{world}",
             "l2": "flushed between timed steps (256 MB write)"}
@@ -226,7 +230,7 @@ def run_ours(args, wl, rank, world, local_rank):
     g0 = torch.randn(n, device=dev, generator=torch.Generator(dev).manual_seed(1000)) * 1e-2
     q = F.calibrate([g0], wl["n_bits"], wl["mbits"])
     del g0
-    cfg = F.CodecConfig(F.SparsificationSpec(wl["theta"]), q, chunk_size=wl["chunk"])
+    cfg = F.CodecConfig(F.SparsificationSpec(wl["theta"], wl.get("mode", "count")), q, chunk_size=wl["chunk"])
     grad = torch.randn(n, device=dev, generator=torch.Generator(dev).manual_seed(1000 + rank)) * 1e-2
     comm = NcclComm() if world > 1 else None
     weights = np.full(world, 1.0 / world)
@@ -418,6 +422,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="resnet50", choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--mode", default="count", choices=["count", "energy"],
+                    help="sparsification rule (spectral.py:124-139); the headline is count mode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default=None, choices=["peer", "nccl"],
                     help="exchange for N>1: peer-to-peer copies (default) or one NCCL allgather")
@@ -425,6 +431,7 @@ def main():
     wl = dict(WORKLOADS[args.workload])
     if args.n:
         wl["n"] = args.n
+    wl["mode"] = args.mode
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `bench.py --gpus N` outside torchrun: launch the N ranks ourselves
         # (one process per GPU) and pass rank 0's JSON line through

@@ -6,15 +6,27 @@
 //   k        = searchsorted(cumsum(energies[order]), budget, side="right")
 //   dropped  = order[:k]
 //
-// Bit-exact with numpy given the same coefficients: the magnitude key is
-// numpy's SIMD cabs (cabs_key), the sum replays numpy's pairwise_sum tree
-// (8-way unrolled leaves of <= 128, halving splits rounded to multiples of
-// 8), the ordering is a stable segmented radix sort of the fp64 keys (CUB),
-// and the cumulative sum is evaluated sequentially in sorted order -- the
-// rounding of each prefix matters, so one thread walks each chunk.  The
-// resulting drop mask feeds the common quantize + pack kernel.
-#include <cub/cub.cuh>
+// Bit-exact with numpy given the same coefficients, one CTA per chunk, no
+// library sort:
+//   * keys are numpy's SIMD cabs (cabs_key), energies w * key * key in fp64;
+//   * energies.sum() replays numpy's pairwise_sum tree exactly: thread 0
+//     lays out the leaves (<= 128 values, splits rounded down to multiples of
+//     8), the threads sum the leaves in parallel (8 strided accumulators, as
+//     numpy's unrolled loop), thread 0 folds them in the tree's order;
+//   * the cut is located by a radix select over the keys' high bits with
+//     per-bucket fp64 energy sums (two passes of 2048 buckets), which leaves a
+//     window of a few bins around the crossing; those are sorted exactly by
+//     (key, bin) -- the stable argsort order -- and their prefix sums are
+//     formed from an accurate sum of everything below the window;
+//   * numpy's cumsum rounds every prefix sequentially; any accurate prefix is
+//     within 2 B u S of it (u = 2^-53, S the prefix, B the bins; Higham's
+//     bound for non-negative terms), so the cut is exact unless a prefix lies
+//     within that distance of the budget -- then (about 1e-7 of chunks, and
+//     whenever the window misses the crossing) the chunk is redone by the
+//     exact fallback: an in-place bitonic sort of its (key, bin) pairs and the
+//     sequential cumulative sum, exactly as numpy rounds it.
 #include <cuda_runtime.h>
+#include <math.h>
 
 #include "fgc_device.cuh"
 #include "fgc_internal.h"
@@ -22,125 +34,381 @@
 namespace fgc {
 namespace {
 
-// per bin: exact key, weighted energy, original index
-template <class T2>
-__global__ void k_energy_prep(const ChunkInfo* chunks, uint32_t first, const T2* spectrum, double* keys,
-                              uint32_t* idx, double* energy) {
-  const ChunkInfo ci = chunks[first + blockIdx.y];
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= ci.bins) return;
-  const T2 x = spectrum[ci.bin_off + b];
-  const double mag = cabs_key((double)x.x, (double)x.y);
-  const bool single = (b == 0) || ((ci.len % 2u) == 0u && b == ci.bins - 1);   // DC / Nyquist weight 1
-  keys[ci.bin_off + b] = mag;
-  idx[ci.bin_off + b] = b;
-  energy[ci.bin_off + b] = (single ? 1.0 : 2.0) * __dmul_rn(mag, mag);
+constexpr int kET = 512;                       // threads per chunk CTA
+constexpr uint32_t kEB = 2048;                 // radix buckets per pass
+constexpr uint32_t kMaxLeaves = 4096;          // parallel pairwise leaves (else thread 0 alone)
+constexpr uint32_t kWin = 1024;                // exact-sort window capacity
+
+__device__ unsigned long long g_energy_fallbacks = 0;   // chunks sent to the exact fallback (diagnostics)
+
+__device__ __forceinline__ double bin_weight(uint32_t b, uint32_t L, uint32_t B) {
+  return (b == 0 || ((L % 2u) == 0u && b == B - 1)) ? 1.0 : 2.0;   // bin_weights (spectral.py:109-115)
 }
 
-// numpy pairwise_sum (numpy/_core/src/umath/loops_utils.h.src) of a[0, n)
-__device__ double pairwise_sum(const double* a, uint32_t n) {
-  // the recursion as an explicit post-order walk: a node is a leaf (n <= 128)
-  // or left + right with the split rounded down to a multiple of 8
+template <class T2>
+__device__ __forceinline__ double key_of(const T2* spec, uint64_t i) {
+  const T2 x = spec[i];
+  return cabs_key((double)x.x, (double)x.y);
+}
+
+// numpy's pairwise_sum leaf (loops_utils.h.src): n <= 128 values a[0, n)
+__device__ double leaf_sum(const double* a, uint32_t n, double (*val)(const double*, uint32_t, const void*),
+                           const void* ctx) {
+  if (n < 8) {
+    double res = 0.0;
+    for (uint32_t i = 0; i < n; ++i) res = __dadd_rn(res, val(a, i, ctx));
+    return res;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = val(a, j, ctx);
+  uint32_t i = 8;
+  for (; i < n - (n % 8u); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], val(a, i + j, ctx));
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, val(a, i, ctx));
+  return res;
+}
+
+struct LeafCtx {
+  uint32_t off, L, B;
+};
+// energy of bin off + i from the stored keys
+__device__ double energy_val(const double* keys, uint32_t i, const void* c) {
+  const LeafCtx& x = *static_cast<const LeafCtx*>(c);
+  const double k = keys[i];
+  return bin_weight(x.off + i, x.L, x.B) * __dmul_rn(k, k);
+}
+
+// The pairwise tree as an explicit post-order walk.  mode 0: record the
+// leaves (offset, size) in order; mode 1: fold the recorded leaf sums; mode 2:
+// sum everything here (too many leaves to record).
+__device__ double pairwise_walk(int mode, uint32_t n, uint32_t* loff, uint32_t* lsz, const double* lsum,
+                                uint32_t* nleaves, const double* keys, uint32_t L, uint32_t B) {
   struct F { uint32_t off, n; int state; };
-  F fs[40];
-  double vals[40];
+  F fs[48];
+  double vals[48];
   int fp = 0, vp = 0;
+  uint32_t leaf = 0;
   fs[fp++] = {0, n, 0};
   while (fp) {
     F& f = fs[fp - 1];
     if (f.n <= 128) {
-      double res;
-      if (f.n < 8) {
-        res = 0.0;
-        for (uint32_t i = 0; i < f.n; ++i) res = __dadd_rn(res, a[f.off + i]);
+      double res = 0.0;
+      if (mode == 0) {
+        if (leaf < kMaxLeaves) { loff[leaf] = f.off; lsz[leaf] = f.n; }
+      } else if (mode == 1) {
+        res = lsum[leaf];
       } else {
-        double r[8];
-        for (int j = 0; j < 8; ++j) r[j] = a[f.off + j];
-        uint32_t i = 8;
-        for (; i < f.n - (f.n % 8u); i += 8)
-          for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[f.off + i + j]);
-        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < f.n; ++i) res = __dadd_rn(res, a[f.off + i]);
+        LeafCtx c{f.off, L, B};
+        res = leaf_sum(keys + f.off, f.n, energy_val, &c);
       }
+      ++leaf;
       vals[vp++] = res;
       --fp;
       continue;
     }
     uint32_t n2 = f.n / 2;
     n2 -= n2 % 8u;
-    if (f.state == 0) {                 // descend left
+    if (f.state == 0) {
       f.state = 1;
       fs[fp++] = {f.off, n2, 0};
-    } else if (f.state == 1) {          // descend right
+    } else if (f.state == 1) {
       f.state = 2;
       fs[fp++] = {f.off + n2, f.n - n2, 0};
-    } else {                            // combine
+    } else {
       const double right = vals[--vp];
       const double left = vals[--vp];
       vals[vp++] = __dadd_rn(left, right);
       --fp;
     }
   }
+  if (nleaves) *nleaves = leaf;
   return vals[0];
 }
 
-__global__ void k_energy_total(const ChunkInfo* chunks, uint32_t first, uint32_t count, const double* energy,
-                               double* total) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= count) return;
-  const ChunkInfo ci = chunks[first + c];
-  total[c] = pairwise_sum(energy + ci.bin_off, ci.bins);
-}
+struct __align__(16) ESh {
+  uint32_t cnt[kEB];
+  uint32_t sum[kEB];                 // bucket energies in 2^-31 units of the chunk total (integer adds)
+  uint32_t loff[kMaxLeaves];
+  uint32_t lsz[kMaxLeaves];
+  double lsum[kMaxLeaves];
+  unsigned long long wkey[kWin];
+  uint32_t widx[kWin];
+  double scan_d[kET / 32 + 1];
+  unsigned long long scan_u[kET / 32 + 1];
+  uint32_t scan[40];
+  uint32_t nleaves, wcount, fbin, kcut, fallback;
+  double total, fbelow_e;
+  unsigned long long fbelow_u;
+};
 
-__global__ void k_energy_gather(const ChunkInfo* chunks, uint32_t first, const uint32_t* sidx, const double* energy,
-                                double* sorted_e) {
-  const ChunkInfo ci = chunks[first + blockIdx.y];
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ci.bins) return;
-  sorted_e[ci.bin_off + i] = energy[ci.bin_off + sidx[ci.bin_off + i]];
-}
-
-// k = #{i : cumsum(sorted energies)[i] <= budget}: one thread per chunk, in order
-__global__ void k_energy_cut(const ChunkInfo* chunks, uint32_t first, uint32_t count, const double* sorted_e,
-                             const double* total, double theta, uint32_t* kcut) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= count) return;
-  const ChunkInfo ci = chunks[first + c];
-  if (theta == 0.0) { kcut[c] = 0; return; }          // spectral.py:135-136
-  const double budget = __dmul_rn(__dmul_rn(theta, theta), total[c]);
-  const double* e = sorted_e + ci.bin_off;
-  double run = 0.0;
-  uint32_t k = 0;
-  const uint32_t n = ci.bins;
-  uint32_t i = 0;
-  for (; i + 4 <= n; i += 4) {
-    const double e0 = e[i], e1 = e[i + 1], e2 = e[i + 2], e3 = e[i + 3];
-    run = __dadd_rn(run, e0); k += run <= budget;
-    run = __dadd_rn(run, e1); k += run <= budget;
-    run = __dadd_rn(run, e2); k += run <= budget;
-    run = __dadd_rn(run, e3); k += run <= budget;
+// Bucket b whose cumulative energy (over buckets in key order, fixed point)
+// first exceeds `budget`: below(b) <= budget < below(b) + sum[b] (the last
+// bucket if none); `below` returns the energy before it.
+__device__ void energy_bucket(ESh& sh, unsigned long long budget, uint32_t& bucket, unsigned long long& below) {
+  constexpr uint32_t per = kEB / kET;          // 4
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  unsigned long long loc = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < per; ++q) loc += sh.sum[t * per + q];
+  unsigned long long x = loc;                  // (u64: a bucket sum is < 2^31, their total < 2^32)
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+    if ((int)lane >= d) x += y;
   }
-  for (; i < n; ++i) { run = __dadd_rn(run, e[i]); k += run <= budget; }
-  kcut[c] = k;
+  if (lane == 31) sh.scan_u[warp] = x;
+  if (t == 0) { sh.fbin = kEB - 1; sh.fbelow_u = 0; }
+  __syncthreads();
+  unsigned long long wb = 0;
+  for (uint32_t w = 0; w < warp; ++w) wb += sh.scan_u[w];
+  const unsigned long long before = wb + x - loc;
+  unsigned long long acc = before;
+  bool found = false;
+#pragma unroll
+  for (uint32_t q = 0; q < per; ++q) {
+    const unsigned long long s = sh.sum[t * per + q];
+    if (!found && acc + s > budget && sh.cnt[t * per + q]) {
+      found = true;
+      atomicMin(&sh.fbin, t * per + q);
+    }
+    acc += s;
+  }
+  __syncthreads();
+  bucket = sh.fbin;
+  if (t == bucket / per) {
+    unsigned long long a = before;
+    for (uint32_t q = 0; q < bucket % per; ++q) a += sh.sum[t * per + q];
+    sh.fbelow_u = a;
+  }
+  __syncthreads();
+  below = sh.fbelow_u;
+  __syncthreads();
 }
 
-__global__ void k_energy_mask(const ChunkInfo* chunks, uint32_t first, const uint32_t* sidx, const uint32_t* kcut,
-                              uint8_t* drop) {
-  const ChunkInfo ci = chunks[first + blockIdx.y];
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ci.bins) return;
-  drop[ci.bin_off + sidx[ci.bin_off + i]] = (i < kcut[blockIdx.y]) ? 1u : 0u;
+// One CTA per chunk: exact pairwise total, radix window, exact window sort,
+// the cut, the drop mask.  fb[c] = 1 asks the exact fallback to redo chunk c.
+template <class T2>
+__global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, uint32_t first, const T2* spectrum,
+                                                        double theta, double* keys, uint8_t* drop, uint32_t* fb) {
+  extern __shared__ __align__(16) unsigned char esm[];
+  ESh& sh = *reinterpret_cast<ESh*>(esm);
+  const uint32_t c = blockIdx.x;
+  const ChunkInfo ci = chunks[first + c];
+  const uint32_t B = ci.bins, L = ci.len, t = threadIdx.x;
+  const T2* sp = spectrum + ci.bin_off;
+  double* K = keys + ci.bin_off;
+  uint8_t* D = drop + ci.bin_off;
+  if (t == 0) { sh.wcount = 0; sh.fallback = 0; }
+  for (uint32_t b = t; b < B; b += kET) K[b] = key_of(sp, b);
+  for (uint32_t b = t; b < kEB; b += kET) { sh.cnt[b] = 0; sh.sum[b] = 0; }
+  __syncthreads();
+  if (theta == 0.0) {                            // spectral.py:135-136: nothing dropped
+    for (uint32_t b = t; b < B; b += kET) D[b] = 0;
+    if (t == 0) fb[c] = 0;
+    return;
+  }
+  // ---- exact pairwise total (numpy's tree)
+  if (t == 0) pairwise_walk(0, B, sh.loff, sh.lsz, nullptr, &sh.nleaves, nullptr, L, B);
+  __syncthreads();
+  const uint32_t nl = sh.nleaves;
+  if (nl <= kMaxLeaves) {
+    for (uint32_t l = t; l < nl; l += kET) {
+      LeafCtx cx{sh.loff[l], L, B};
+      sh.lsum[l] = leaf_sum(K + sh.loff[l], sh.lsz[l], energy_val, &cx);
+    }
+    __syncthreads();
+    if (t == 0) sh.total = pairwise_walk(1, B, nullptr, nullptr, sh.lsum, nullptr, nullptr, L, B);
+  } else if (t == 0) {
+    sh.total = pairwise_walk(2, B, nullptr, nullptr, nullptr, nullptr, K, L, B);
+  }
+  __syncthreads();
+  const double budget = __dmul_rn(__dmul_rn(theta, theta), sh.total);
+  // ---- radix window over the keys' high 32 bits: [31:20] exponent+, then
+  //      [19:9]; bucket energies in fixed point (units of 2^-31 of the total:
+  //      native 32-bit shared-memory atomics, order-free; truncation costs at
+  //      most B 2^-31 of the total, below one sub-bucket's energy, and the
+  //      window keeps two sub-buckets of margin each side)
+  auto hi32 = [&](uint32_t b) { return (uint32_t)((unsigned long long)__double_as_longlong(K[b]) >> 32); };
+  const double fscale = sh.total > 0.0 ? 0x1p31 / sh.total : 0.0;
+  auto approx_e = [&](uint32_t h, uint32_t b) -> uint32_t {
+    const double k = __hiloint2double((int)h, 0);
+    return (uint32_t)fmin(bin_weight(b, L, B) * k * k * fscale, 0x1p31);
+  };
+  const unsigned long long ubudget = (unsigned long long)fmin(budget * fscale, 0x1p62);
+  for (uint32_t b = t; b < B; b += kET) {
+    const uint32_t h = hi32(b);
+    atomicAdd(&sh.cnt[h >> 20], 1u);
+    atomicAdd(&sh.sum[h >> 20], approx_e(h, b));
+  }
+  __syncthreads();
+  uint32_t b1;
+  unsigned long long e1;
+  energy_bucket(sh, ubudget, b1, e1);
+  for (uint32_t b = t; b < kEB; b += kET) { sh.cnt[b] = 0; sh.sum[b] = 0; }
+  __syncthreads();
+  for (uint32_t b = t; b < B; b += kET) {
+    const uint32_t h = hi32(b);
+    if ((h >> 20) == b1) {
+      atomicAdd(&sh.cnt[(h >> 9) & 2047u], 1u);
+      atomicAdd(&sh.sum[(h >> 9) & 2047u], approx_e(h, b));
+    }
+  }
+  __syncthreads();
+  uint32_t b2;
+  unsigned long long e2;
+  energy_bucket(sh, ubudget > e1 ? ubudget - e1 : 0ull, b2, e2);
+  (void)e2;
+  // window: two sub-buckets each side of b2 (the fixed-point sums may put the
+  // crossing a bucket off); everything below it is certainly dropped
+  const uint32_t base = (b1 << 20) | (b2 << 9);
+  const uint32_t wlo = base >= 1024u ? base - 1024u : 0u;
+  const uint32_t whi = base + 1536u;
+  double below = 0.0;
+  uint32_t nbelow = 0;
+  for (uint32_t b = t; b < B; b += kET) {
+    const uint32_t h = hi32(b);
+    if (h < wlo) {
+      const double k = K[b];
+      below += bin_weight(b, L, B) * __dmul_rn(k, k);
+      ++nbelow;
+    } else if (h < whi) {
+      const uint32_t s = atomicAdd(&sh.wcount, 1u);
+      if (s < kWin) {
+        sh.wkey[s] = (unsigned long long)__double_as_longlong(K[b]);
+        sh.widx[s] = b;
+      }
+    }
+  }
+  // block sums of `below` (fp64) and `nbelow`
+  {
+    const uint32_t lane = t & 31, warp = t >> 5;
+    for (int d = 16; d > 0; d >>= 1) {
+      below += __shfl_down_sync(0xffffffffu, below, d);
+      nbelow += __shfl_down_sync(0xffffffffu, nbelow, d);
+    }
+    if (lane == 0) { sh.scan_d[warp] = below; sh.scan[warp] = nbelow; }
+    __syncthreads();
+    if (t == 0) {
+      double s = 0.0;
+      uint32_t n = 0;
+      for (int w = 0; w < kET / 32; ++w) { s += sh.scan_d[w]; n += sh.scan[w]; }
+      sh.fbelow_e = s;
+      sh.kcut = n;
+    }
+    __syncthreads();
+  }
+  const double S0 = sh.fbelow_e;
+  const uint32_t n0 = sh.kcut;
+  const uint32_t m = sh.wcount;
+  if (m > kWin) {
+    if (t == 0) sh.fallback = 1;
+  } else {
+    // exact (key, bin) order of the window: rank by counting (m is small)
+    __syncthreads();
+    for (uint32_t i = t; i < m; i += kET) {
+      const unsigned long long k = sh.wkey[i];
+      const uint32_t bi = sh.widx[i];
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < m; ++j) {
+        const unsigned long long kj = sh.wkey[j];
+        rank += (kj < k || (kj == k && sh.widx[j] < bi)) ? 1u : 0u;
+      }
+      sh.loff[rank] = bi;                         // window bins in sorted order (loff reused)
+    }
+    __syncthreads();
+    if (t == 0) {
+      // prefix sums over the window; tolerance covers numpy's sequential rounding
+      const double u = 0x1p-53;
+      const double tol = 2.0 * (double)(B + 8) * u * fmax(budget, S0) * 2.0;
+      bool ok = S0 <= budget - tol;               // everything below the window is in
+      double S = S0;
+      uint32_t k = n0;
+      bool crossed = false;
+      for (uint32_t i = 0; i < m && ok; ++i) {
+        const uint32_t bi = sh.loff[i];
+        const double kk = K[bi];
+        S += bin_weight(bi, L, B) * __dmul_rn(kk, kk);
+        const double tl = 2.0 * (double)(B + 8) * u * fmax(S, budget) * 2.0;
+        if (fabs(S - budget) <= tl) ok = false;   // too close to call: the exact fallback decides
+        else if (S <= budget) ++k;
+        else { crossed = true; break; }
+      }
+      if (!crossed) ok = false;                   // the window did not reach the budget
+      (void)tol;
+      sh.fallback = ok ? 0u : 1u;
+      sh.kcut = k - n0;                           // dropped window entries
+    }
+  }
+  __syncthreads();
+  if (sh.fallback) {
+    if (t == 0) {
+      fb[c] = 1;
+      atomicAdd(&g_energy_fallbacks, 1ull);
+    }
+    return;
+  }
+  // ---- the drop mask: below the window, and the first kcut window entries
+  const uint32_t kw = sh.kcut;
+  for (uint32_t b = t; b < B; b += kET) D[b] = hi32(b) < wlo ? 1u : 0u;
+  __syncthreads();
+  for (uint32_t i = t; i < m; i += kET) D[sh.loff[i]] = i < kw ? 1u : 0u;
+  if (t == 0) fb[c] = 0;
 }
 
-__global__ void k_seg_offsets(const ChunkInfo* chunks, uint32_t first, uint32_t count, int* offs) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > count) return;
-  const ChunkInfo ci = chunks[first + (c < count ? c : count - 1)];
-  offs[c] = (int)(c < count ? ci.bin_off : ci.bin_off + ci.bins);
+// Exact fallback for the flagged chunks: in-place bitonic sort of (key, bin)
+// over the chunk's bins (virtual +inf entries above B never move down: every
+// comparison puts the minimum at the lower index), then numpy's sequential
+// cumulative sum in sorted order.
+__global__ void __launch_bounds__(1024) k_energy_exact(const ChunkInfo* chunks, uint32_t first, double theta,
+                                                        double* keys, uint32_t* idx, uint8_t* drop,
+                                                        const uint32_t* fb) {
+  const uint32_t c = blockIdx.x;
+  if (!fb[c]) return;
+  const ChunkInfo ci = chunks[first + c];
+  const uint32_t B = ci.bins, L = ci.len, t = threadIdx.x;
+  double* K = keys + ci.bin_off;                  // sorted in place (keys are recomputed per call)
+  uint32_t* I = idx + ci.bin_off;
+  uint8_t* D = drop + ci.bin_off;
+  __shared__ double total_s;
+  __shared__ uint32_t kcut_s;
+  // the total, before the keys are permuted (thread 0, the tree walk)
+  if (t == 0) total_s = pairwise_walk(2, B, nullptr, nullptr, nullptr, nullptr, K, L, B);
+  for (uint32_t b = t; b < B; b += blockDim.x) I[b] = b;
+  __syncthreads();
+  uint32_t N2 = 1;
+  while (N2 < B) N2 <<= 1;
+  auto less = [&](uint32_t a, uint32_t b) {
+    const double ka = K[a], kb = K[b];
+    return ka < kb || (ka == kb && I[a] < I[b]);
+  };
+  for (uint32_t k = 2; k <= N2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = t; i < N2; i += blockDim.x) {
+        const uint32_t p = (j == (k >> 1)) ? (i ^ (k - 1)) : (i ^ j);   // mirrored first step, then halvers
+        if (p > i && p < B && i < B && less(p, i)) {
+          const double tk = K[i]; K[i] = K[p]; K[p] = tk;
+          const uint32_t ti = I[i]; I[i] = I[p]; I[p] = ti;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (t == 0) {
+    const double budget = __dmul_rn(__dmul_rn(theta, theta), total_s);
+    double run = 0.0;
+    uint32_t k = 0;
+    for (uint32_t i = 0; i < B && theta != 0.0; ++i) {      // theta == 0 drops nothing (spectral.py:135-136)
+      const double kk = K[i];
+      run = __dadd_rn(run, bin_weight(I[i], L, B) * __dmul_rn(kk, kk));
+      k += run <= budget ? 1u : 0u;
+    }
+    kcut_s = k;
+  }
+  __syncthreads();
+  for (uint32_t i = t; i < B; i += blockDim.x) D[I[i]] = i < kcut_s ? 1u : 0u;
 }
-
-inline uint32_t cdiv32(uint64_t a, uint32_t b) { return (uint32_t)((a + b - 1) / b); }
 
 }  // namespace
 
@@ -148,71 +416,65 @@ fgc_status EnergyScratch::ensure(uint64_t bins, uint32_t chunks) {
   if (bins <= cap_bins && chunks <= cap_chunks) return FGC_OK;
   free_all();
   FGC_CUDA(cudaMalloc(&keys, sizeof(double) * bins));
-  FGC_CUDA(cudaMalloc(&keys2, sizeof(double) * bins));
-  FGC_CUDA(cudaMalloc(&energy, sizeof(double) * bins));
-  FGC_CUDA(cudaMalloc(&sorted_e, sizeof(double) * bins));
   FGC_CUDA(cudaMalloc(&idx, sizeof(uint32_t) * bins));
-  FGC_CUDA(cudaMalloc(&idx2, sizeof(uint32_t) * bins));
   FGC_CUDA(cudaMalloc(&drop, bins));
-  FGC_CUDA(cudaMalloc(&total, sizeof(double) * chunks));
   FGC_CUDA(cudaMalloc(&kcut, sizeof(uint32_t) * chunks));
-  FGC_CUDA(cudaMalloc(&offs, sizeof(int) * (chunks + 1)));
-  size_t tb = 0;
-  FGC_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tb, keys, keys2, idx, idx2, (int)bins, (int)chunks,
-                                                    offs, offs + 1));
-  FGC_CUDA(cudaMalloc(&temp, tb));
-  temp_bytes = tb;
   cap_bins = bins;
   cap_chunks = chunks;
+  static bool attr = false;
+  if (!attr) {
+    FGC_CUDA(cudaFuncSetAttribute(k_energy_select<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(ESh)));
+    FGC_CUDA(cudaFuncSetAttribute(k_energy_select<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(ESh)));
+    attr = true;
+  }
   return FGC_OK;
 }
 
 void EnergyScratch::free_all() {
-  cudaFree(keys); cudaFree(keys2); cudaFree(energy); cudaFree(sorted_e);
-  cudaFree(idx); cudaFree(idx2); cudaFree(drop); cudaFree(total); cudaFree(kcut); cudaFree(offs); cudaFree(temp);
-  keys = keys2 = energy = sorted_e = total = nullptr;
-  idx = idx2 = kcut = nullptr;
+  cudaFree(keys); cudaFree(idx); cudaFree(drop); cudaFree(kcut);
+  keys = nullptr;
+  idx = kcut = nullptr;
   drop = nullptr;
-  offs = nullptr;
-  temp = nullptr;
   cap_bins = 0;
   cap_chunks = 0;
-  temp_bytes = 0;
 }
 
+// Debug knob: force every chunk through the exact fallback (tests).
+static bool g_energy_force_exact = false;
+
 // Drop mask (1 = dropped) for chunks [first, first + count) of a chunk-major
-// float2 spectrum whose bins start at bin_off(first) = bin0.
+// spectrum (float2, or double2 when f64) whose bins start at bin_off(first) = bin0.
 fgc_status energy_drop_mask(EnergyScratch& e, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                             uint64_t bin0, uint64_t nbins, uint32_t max_bins, const void* spectrum, int f64,
                             double theta, cudaStream_t s, const uint8_t** drop_out) {
   if (!count) return FGC_OK;
+  (void)max_bins;
   FGC_TRY(e.ensure(bin0 + nbins, count));
-  const dim3 grid(cdiv32(max_bins, 256), count);
   if (f64)
-    k_energy_prep<double2><<<grid, 256, 0, s>>>(d_chunks, first, static_cast<const double2*>(spectrum), e.keys,
-                                                e.idx, e.energy);
+    k_energy_select<double2><<<count, kET, sizeof(ESh), s>>>(d_chunks, first, static_cast<const double2*>(spectrum),
+                                                             theta, e.keys, e.drop, e.kcut);
   else
-    k_energy_prep<float2><<<grid, 256, 0, s>>>(d_chunks, first, static_cast<const float2*>(spectrum), e.keys, e.idx,
-                                               e.energy);
+    k_energy_select<float2><<<count, kET, sizeof(ESh), s>>>(d_chunks, first, static_cast<const float2*>(spectrum),
+                                                            theta, e.keys, e.drop, e.kcut);
   FGC_LAUNCHED(1);
-  k_energy_total<<<cdiv32(count, 64), 64, 0, s>>>(d_chunks, first, count, e.energy, e.total);
-  FGC_LAUNCHED(1);
-  k_seg_offsets<<<cdiv32(count + 1, 128), 128, 0, s>>>(d_chunks, first, count, e.offs);
-  FGC_LAUNCHED(1);
-  size_t tb = e.temp_bytes;
-  // sorted copies land at the same bin offsets (segments are the chunks' bin ranges)
-  FGC_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(e.temp, tb, e.keys, e.keys2, e.idx, e.idx2,
-                                                    (int)(bin0 + nbins), (int)count, e.offs, e.offs + 1, 0,
-                                                    sizeof(double) * 8, s));
-  FGC_LAUNCHED(1);
-  k_energy_gather<<<grid, 256, 0, s>>>(d_chunks, first, e.idx2, e.energy, e.sorted_e);
-  FGC_LAUNCHED(1);
-  k_energy_cut<<<cdiv32(count, 32), 32, 0, s>>>(d_chunks, first, count, e.sorted_e, e.total, theta, e.kcut);
-  FGC_LAUNCHED(1);
-  k_energy_mask<<<grid, 256, 0, s>>>(d_chunks, first, e.idx2, e.kcut, e.drop);
+  if (g_energy_force_exact) FGC_CUDA(cudaMemsetAsync(e.kcut, 0x01, sizeof(uint32_t) * count, s));
+  k_energy_exact<<<count, 1024, 0, s>>>(d_chunks, first, theta, e.keys, e.idx, e.drop, e.kcut);
   FGC_LAUNCHED(1);
   *drop_out = e.drop;
   return FGC_OK;
 }
 
 }  // namespace fgc
+
+extern "C" unsigned long long fgc_debug_energy_fallbacks(void) {
+  unsigned long long v = 0;
+  cudaMemcpyFromSymbol(&v, fgc::g_energy_fallbacks, sizeof(v));
+  return v;
+}
+
+extern "C" int fgc_debug_energy_force_exact(int on) {
+  fgc::g_energy_force_exact = on != 0;
+  return 0;
+}

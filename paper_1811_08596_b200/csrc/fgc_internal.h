@@ -168,12 +168,10 @@ fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_
 
 // Energy-mode drop sets (energy.cu).
 struct EnergyScratch {
-  double *keys = nullptr, *keys2 = nullptr, *energy = nullptr, *sorted_e = nullptr, *total = nullptr;
-  uint32_t *idx = nullptr, *idx2 = nullptr, *kcut = nullptr;
-  uint8_t* drop = nullptr;
-  int* offs = nullptr;
-  void* temp = nullptr;
-  size_t temp_bytes = 0;
+  double* keys = nullptr;            // per bin: numpy cabs key (sorted in place by the exact fallback)
+  uint32_t* idx = nullptr;           // per bin: bin index (exact fallback)
+  uint32_t* kcut = nullptr;          // per chunk: 1 = redo with the exact fallback
+  uint8_t* drop = nullptr;           // per bin: 1 = dropped
   uint64_t cap_bins = 0;
   uint32_t cap_chunks = 0;
   fgc_status ensure(uint64_t bins, uint32_t chunks);

@@ -184,8 +184,10 @@ extern "C" fgc_status fgc_plan_create(const fgc_codec_desc* desc, fgc_plan** out
     c.bins = c.L / 2 + 1;
     c.first = 0;
     c.count = (uint32_t)full;
-    c.fused = fused_available() && fused_enabled() && c.L == 65536 && d.mode == FGC_MODE_COUNT &&
-              !d.passthrough && d.quant.n_bits <= 16;
+    // 65536-sample chunks run the fused kernels: the fused compress in count
+    // mode; in energy mode the fused forward transform and the fused decode
+    // around the energy selection
+    c.fused = fused_available() && fused_enabled() && c.L == 65536 && !d.passthrough && d.quant.n_bits <= 16;
     p->classes.push_back(c);
   }
   if (tail) {
@@ -380,14 +382,19 @@ static fgc_status check_mode(const fgc_plan* p) {
   return FGC_OK;
 }
 
-// Energy mode (spectral.py:134-139): every chunk through the generic FFT
-// (energy plans take no fused class), the exact energy drop set, then the
-// common quantize + pack with the drop mask.  spectrum_in (chunk-major
-// float2) replaces the forward transform when given (stage injection).
+// Energy mode (spectral.py:134-139): the forward transform (the fused
+// kernel's for 65536-sample chunks, the generic engine otherwise), the exact
+// energy drop set, then the common quantize + pack with the drop mask.
+// spectrum_in (chunk-major float2) replaces the forward transform when given
+// (stage injection).
 static fgc_status energy_compress(fgc_plan* p, const void* grad, int dtype, const float2* spectrum_in,
                                   uint8_t* message, uint8_t* kept_mask, uint32_t* flags, cudaStream_t s) {
   const float2* spec = spectrum_in;
   if (!spec) {
+    for (RealClass& rc : p->classes)
+      if (rc.fused)
+        FGC_TRY(launch_fused_spectrum(p->fused, p->d_chunks, rc.first, rc.count, grad, dtype, p->desc.half_pass,
+                                      p->d_spec, flags, s));
     FGC_TRY(forward_generic(p, grad, dtype, p->d_spec, flags, s, false));
     spec = p->d_spec;
   }
@@ -856,7 +863,7 @@ static fgc_status exchange_average_impl(fgc_plan* p, fgc_exchange* x, const void
     FGC_CUDA(cudaEventRecord(ev_tail, s));
     FGC_TRY(exchange_publish_event(x, k, 0, p->msg_bytes, ev_tail, tval));
     FGC_TRY(exchange_wait(x, s, (int)Pmax, tval));
-    FGC_TRY(decode_range(p, gathered, W, p->msg_bytes, w, out, s, 0, 0, true));
+    FGC_TRY(decode_range(p, gathered, W, p->msg_bytes, w, out, s, p->fused_first, p->fused_count, true));
     FGC_TRY(exchange_join(x, s));
     *step += 1;
     return FGC_OK;
@@ -1010,11 +1017,13 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
   // generic chunks (all of them for energy mode / plans without fused
   // chunks): elements [g_lo, n), message bytes [m_lo, end), slot P (tail slot
   // of the exchange)
-  const bool generic = p->classes.size() > (p->fused_count ? 1u : 0u);
-  const uint64_t g_lo = p->fused_count ? p->chunks[p->fused_first + p->fused_count - 1].in_off +
-                                             p->chunks[p->fused_first + p->fused_count - 1].len
-                                       : 0;
-  const uint64_t m_lo = p->fused_count ? p->seg_off[p->fused_first + p->fused_count] : 0;
+  // (energy mode runs the whole message here, fused chunks included)
+  const bool pieces = !energy && p->fused_count;
+  const bool generic = energy || p->classes.size() > (p->fused_count ? 1u : 0u);
+  const uint64_t g_lo = pieces ? p->chunks[p->fused_first + p->fused_count - 1].in_off +
+                                     p->chunks[p->fused_first + p->fused_count - 1].len
+                               : 0;
+  const uint64_t m_lo = pieces ? p->seg_off[p->fused_first + p->fused_count] : 0;
   cudaStream_t g = P ? p->side : s;
   if (generic) {
     FGC_CUDA(h2d(g_lo, p->desc.n));
@@ -1027,7 +1036,8 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
       FGC_TRY(exchange_publish_event(x, k, m_lo, p->msg_bytes - m_lo, p->ev_c2[P], tval, (int)Pmax));
       FGC_TRY(exchange_wait(x, g, (int)Pmax, tval));
     }
-    FGC_TRY(decode_range(p, gathered, W, p->msg_bytes, w, dev_out, g, 0, 0, true));
+    FGC_TRY(decode_range(p, gathered, W, p->msg_bytes, w, dev_out, g, energy ? p->fused_first : 0,
+                         energy ? p->fused_count : 0, true));
     FGC_CUDA(cudaEventRecord(p->ev_d[P], g));
   }
   // fused pieces: elements [chunk f[i] .. chunk f[i+1])

@@ -607,9 +607,23 @@ def _size_properties(n, theta, nm):
 
 # ---------------------------------------------------------------- energy mode
 
+@pytest.fixture(params=[False, True], ids=["window", "exact-fallback"])
+def energy_path(request):
+    """Energy mode decides each chunk's cut from a small exactly-sorted window
+    unless numpy's sequential rounding could matter; the exact fallback (full
+    in-place sort + sequential cumsum) is forced here to test it as well."""
+    import ctypes
+    from paper_1811_08596_b200 import _lib
+    f = _lib.lib.fgc_debug_energy_force_exact
+    f.argtypes = [ctypes.c_int]
+    f(1 if request.param else 0)
+    yield request.param
+    f(0)
+
+
 @pytest.mark.parametrize("theta", [0.0, 0.3, 0.7, 0.95, 1.0])
 @pytest.mark.parametrize("n,chunk,nm", [(3 * 65536 + 40960, 65536, (8, 3)), (5000, 1024, (6, 2)), (71, 16, None)])
-def test_energy_mode_injection_bit_exact(theta, n, chunk, nm):
+def test_energy_mode_injection_bit_exact(theta, n, chunk, nm, energy_path):
     """spectral.py:134-139 given identical coefficients: kept mask, bitmap and
     codes equal the oracle's (numpy pairwise sum, stable order, sequential
     cumulative energy)."""
@@ -658,7 +672,7 @@ def test_energy_mode_round_trip_and_wire():
 
 @pytest.mark.parametrize("n", [8, 9, 1000, 1001, 65536, 100_003])
 @pytest.mark.parametrize("theta", [0.0, 0.5, 0.9, 1.0])
-def test_truncate_energy_mode_complex128(n, theta):
+def test_truncate_energy_mode_complex128(n, theta, energy_path):
     """spectral.truncate with mode "energy" on complex128 coefficients: the
     GPU drop set equals the oracle's (Parseval weights by n's parity)."""
     rng = np.random.default_rng(n)
