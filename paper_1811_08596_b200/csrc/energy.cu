@@ -36,7 +36,8 @@ namespace {
 
 constexpr int kET = 512;                       // threads per chunk CTA
 constexpr uint32_t kEB = 2048;                 // radix buckets per pass
-constexpr uint32_t kMaxLeaves = 4096;          // parallel pairwise leaves (else thread 0 alone)
+constexpr uint32_t kTreeDepth = 10;            // parallel pairwise tree depth (else thread 0 alone)
+constexpr uint32_t kTreeNodes = (2u << kTreeDepth) - 1;   // heap of levels 0..kTreeDepth
 constexpr uint32_t kWin = 1024;                // exact-sort window capacity
 
 __device__ unsigned long long g_energy_fallbacks = 0;   // chunks sent to the exact fallback (diagnostics)
@@ -80,9 +81,8 @@ __device__ double energy_val(const double* keys, uint32_t i, const void* c) {
   return bin_weight(x.off + i, x.L, x.B) * __dmul_rn(k, k);
 }
 
-// The pairwise tree as an explicit post-order walk.  mode 0: record the
-// leaves (offset, size) in order; mode 1: fold the recorded leaf sums; mode 2:
-// sum everything here (too many leaves to record).
+// The pairwise tree as an explicit post-order walk by one thread (mode 2:
+// sum everything here; used when the tree is deeper than the parallel heap).
 __device__ double pairwise_walk(int mode, uint32_t n, uint32_t* loff, uint32_t* lsz, const double* lsum,
                                 uint32_t* nleaves, const double* keys, uint32_t L, uint32_t B) {
   struct F { uint32_t off, n; int state; };
@@ -95,11 +95,7 @@ __device__ double pairwise_walk(int mode, uint32_t n, uint32_t* loff, uint32_t* 
     F& f = fs[fp - 1];
     if (f.n <= 128) {
       double res = 0.0;
-      if (mode == 0) {
-        if (leaf < kMaxLeaves) { loff[leaf] = f.off; lsz[leaf] = f.n; }
-      } else if (mode == 1) {
-        res = lsum[leaf];
-      } else {
+      {
         LeafCtx c{f.off, L, B};
         res = leaf_sum(keys + f.off, f.n, energy_val, &c);
       }
@@ -130,15 +126,15 @@ __device__ double pairwise_walk(int mode, uint32_t n, uint32_t* loff, uint32_t* 
 struct __align__(16) ESh {
   uint32_t cnt[kEB];
   uint32_t sum[kEB];                 // bucket energies in 2^-31 units of the chunk total (integer adds)
-  uint32_t loff[kMaxLeaves];
-  uint32_t lsz[kMaxLeaves];
-  double lsum[kMaxLeaves];
+  uint32_t hoff[kTreeNodes];         // numpy's pairwise tree as a heap: node i -> children 2i+1, 2i+2
+  uint32_t hn[kTreeNodes];           // node size (0: absent)
+  double hval[kTreeNodes];           // node sums
   unsigned long long wkey[kWin];
   uint32_t widx[kWin];
   double scan_d[kET / 32 + 1];
   unsigned long long scan_u[kET / 32 + 1];
   uint32_t scan[40];
-  uint32_t nleaves, wcount, fbin, kcut, fallback;
+  uint32_t wcount, fbin, kcut, fallback;
   double total, fbelow_e;
   unsigned long long fbelow_u;
 };
@@ -209,17 +205,49 @@ __global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, 
     if (t == 0) fb[c] = 0;
     return;
   }
-  // ---- exact pairwise total (numpy's tree)
-  if (t == 0) pairwise_walk(0, B, sh.loff, sh.lsz, nullptr, &sh.nleaves, nullptr, L, B);
+  // ---- exact pairwise total: numpy's tree (split n > 128 at n/2 rounded
+  //      down to a multiple of 8) built level by level as a heap, the leaves
+  //      summed in parallel, the inner nodes folded bottom-up (left + right)
+  if (t == 0) { sh.hoff[0] = 0; sh.hn[0] = B; }
   __syncthreads();
-  const uint32_t nl = sh.nleaves;
-  if (nl <= kMaxLeaves) {
-    for (uint32_t l = t; l < nl; l += kET) {
-      LeafCtx cx{sh.loff[l], L, B};
-      sh.lsum[l] = leaf_sum(K + sh.loff[l], sh.lsz[l], energy_val, &cx);
+  uint32_t depth = 0;
+  bool deeper = B > 128;
+  while (deeper && depth < kTreeDepth) {
+    const uint32_t l0 = (1u << depth) - 1, cnt = 1u << depth;
+    bool split = false;
+    for (uint32_t i = t; i < cnt; i += kET) {
+      const uint32_t nd = l0 + i, n = sh.hn[nd];
+      uint32_t n2 = n / 2;
+      n2 -= n2 % 8u;
+      const bool inner = n > 128;
+      sh.hoff[2 * nd + 1] = sh.hoff[nd];
+      sh.hn[2 * nd + 1] = inner ? n2 : 0u;
+      sh.hoff[2 * nd + 2] = sh.hoff[nd] + n2;
+      sh.hn[2 * nd + 2] = inner ? n - n2 : 0u;
+      split |= inner && (n2 > 128 || n - n2 > 128);
+    }
+    ++depth;
+    deeper = __syncthreads_or(split);
+  }
+  if (!deeper) {
+    const uint32_t nodes = (2u << depth) - 1;
+    for (uint32_t nd = t; nd < nodes; nd += kET) {
+      const uint32_t n = sh.hn[nd];
+      if (n && n <= 128) {
+        LeafCtx cx{sh.hoff[nd], L, B};
+        sh.hval[nd] = leaf_sum(K + sh.hoff[nd], n, energy_val, &cx);
+      }
     }
     __syncthreads();
-    if (t == 0) sh.total = pairwise_walk(1, B, nullptr, nullptr, sh.lsum, nullptr, nullptr, L, B);
+    for (int l = (int)depth - 1; l >= 0; --l) {
+      const uint32_t l0 = (1u << l) - 1, cnt = 1u << l;
+      for (uint32_t i = t; i < cnt; i += kET) {
+        const uint32_t nd = l0 + i;
+        if (sh.hn[nd] > 128) sh.hval[nd] = __dadd_rn(sh.hval[2 * nd + 1], sh.hval[2 * nd + 2]);
+      }
+      __syncthreads();
+    }
+    if (t == 0) sh.total = sh.hval[0];
   } else if (t == 0) {
     sh.total = pairwise_walk(2, B, nullptr, nullptr, nullptr, nullptr, K, L, B);
   }
@@ -315,7 +343,7 @@ __global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, 
         const unsigned long long kj = sh.wkey[j];
         rank += (kj < k || (kj == k && sh.widx[j] < bi)) ? 1u : 0u;
       }
-      sh.loff[rank] = bi;                         // window bins in sorted order (loff reused)
+      sh.hoff[rank] = bi;                         // window bins in sorted order (the tree heap is free)
     }
     __syncthreads();
     if (t == 0) {
@@ -327,7 +355,7 @@ __global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, 
       uint32_t k = n0;
       bool crossed = false;
       for (uint32_t i = 0; i < m && ok; ++i) {
-        const uint32_t bi = sh.loff[i];
+        const uint32_t bi = sh.hoff[i];
         const double kk = K[bi];
         S += bin_weight(bi, L, B) * __dmul_rn(kk, kk);
         const double tl = 2.0 * (double)(B + 8) * u * fmax(S, budget) * 2.0;
@@ -353,7 +381,7 @@ __global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, 
   const uint32_t kw = sh.kcut;
   for (uint32_t b = t; b < B; b += kET) D[b] = hi32(b) < wlo ? 1u : 0u;
   __syncthreads();
-  for (uint32_t i = t; i < m; i += kET) D[sh.loff[i]] = i < kw ? 1u : 0u;
+  for (uint32_t i = t; i < m; i += kET) D[sh.hoff[i]] = i < kw ? 1u : 0u;
   if (t == 0) fb[c] = 0;
 }
 
