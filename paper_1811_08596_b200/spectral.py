@@ -1,10 +1,12 @@
-"""Real DFT and count-mode magnitude truncation -- drop-in for the hot-path
-part of ``fgc.spectral`` (pkg/src/fgc/spectral.py).
+"""Real DFT and magnitude truncation -- drop-in for the hot-path part of
+``fgc.spectral`` (pkg/src/fgc/spectral.py).
 
 ``dft_forward`` / ``dft_inverse`` run a float64 GPU DFT (any length, like
-numpy's pocketfft); ``truncate`` runs the GPU count-mode selection with
-numpy's exact complex-abs key and the stable index tie-break.  Energy mode
-and the time-domain audit helpers are outside this build's scope.
+numpy's pocketfft); ``truncate`` runs the GPU selection -- count mode, or
+energy mode (numpy's pairwise total, stable order and sequential cumulative
+energy, csrc/energy.cu) -- with numpy's exact complex-abs key and the stable
+index tie-break.  The time-domain audit helpers (``sparsify_time``,
+``assumption_check``) are outside this build's scope.
 """
 
 from __future__ import annotations
