@@ -177,6 +177,15 @@ fgc_status fgc_decode_average(fgc_plan* plan, const uint8_t* messages, int W,
                               uint64_t message_stride, const double* weights, float* out,
                               void* stream);
 
+/* Sender-side reconstruction error by Parseval (the simulator's err_ratio,
+ * simulator.py:538-542, without a decode): given a chunk-major float2
+ * spectrum (fgc_forward_spectrum) and the message compress() made from it,
+ * err_norm[2c], err_norm[2c+1] (device doubles) = ||x - decompress(m)||^2 and
+ * ||x||^2 of chunk c, from (1/L) sum_k w_k |X_k - Xhat_k|^2 and
+ * (1/L) sum_k w_k |X_k|^2 (Parseval weights, spectral.py:109-115). */
+fgc_status fgc_spectrum_error(fgc_plan* plan, const void* spectrum, const uint8_t* message, double* err_norm,
+                              void* stream);
+
 /* Debug hook: the averaged spectrum before the inverse FFT (float2). */
 fgc_status fgc_decode_spectrum(fgc_plan* plan, const uint8_t* messages, int W,
                                uint64_t message_stride, const double* weights, void* spectrum,

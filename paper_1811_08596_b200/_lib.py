@@ -68,6 +68,7 @@ _SIGS = {
     "fgc_decode_average": (I32, [P, P, I32, U64, P, P, P]),
     "fgc_decode_spectrum": (I32, [P, P, I32, U64, P, P, P]),
     "fgc_inverse_spectrum": (I32, [P, P, P, P]),
+    "fgc_spectrum_error": (I32, [P, P, P, P, P]),
     "fgc_serialize": (I32, [P, P, P, P, P]),
     "fgc_parse_header": (I32, [P, U64, C.POINTER(CodecDesc)]),
     "fgc_wire_index": (I32, [P, U64, C.POINTER(CodecDesc), P, P, C.POINTER(U32)]),

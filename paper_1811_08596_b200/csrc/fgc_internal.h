@@ -189,6 +189,11 @@ fgc_status launch_decode_accumulate(const ChunkInfo* d_chunks, uint32_t first, u
                                     const uint8_t* messages, int W, uint64_t stride, const Weights& wts,
                                     const QuantParams& q, float2* spectrum, uint32_t max_slots, cudaStream_t s);
 
+// Parseval reconstruction error per chunk: out[c] = (err, norm) of chunk c.
+fgc_status launch_spectrum_error(const ChunkInfo* d_chunks, uint32_t n_chunks, uint32_t max_slots,
+                                 const float2* spectrum, const uint8_t* message, const QuantParams& q, double2* out,
+                                 cudaStream_t s);
+
 // Wire format kernels (wire.cu).
 fgc_status launch_serialize(const ChunkInfo* d_chunks, uint32_t n_chunks, const uint8_t* message, int n_bits,
                             const uint8_t header[FGC_HEADER_BYTES], uint8_t* wire, uint64_t* wire_len,

@@ -535,6 +535,19 @@ extern "C" fgc_status fgc_decode_spectrum(fgc_plan* p, const uint8_t* messages, 
                                   static_cast<float2*>(spectrum), p->max_slots, static_cast<cudaStream_t>(stream));
 }
 
+extern "C" fgc_status fgc_spectrum_error(fgc_plan* p, const void* spectrum, const uint8_t* message,
+                                         double* err_norm, void* stream) {
+  if (!p || !spectrum || !message || !err_norm) { set_error("null argument"); return FGC_ERR_INVALID; }
+  FGC_TRY(check_messages(message, 16));
+  if (p->q.n_bits == 32) {
+    set_error("the Parseval error needs a quantizer (passthrough codes are the coefficients)");
+    return FGC_ERR_UNSUPPORTED;
+  }
+  return launch_spectrum_error(p->d_chunks, p->n_chunks, p->max_slots, static_cast<const float2*>(spectrum),
+                               message, p->q, reinterpret_cast<double2*>(err_norm),
+                               static_cast<cudaStream_t>(stream));
+}
+
 extern "C" fgc_status fgc_inverse_spectrum(fgc_plan* p, const void* spectrum, float* out, void* stream) {
   if (!p || !spectrum || !out) { set_error("null argument"); return FGC_ERR_INVALID; }
   FGC_TRY(check_out(out));

@@ -906,3 +906,24 @@ def test_pack_unpack_dtypes():
         np.testing.assert_array_equal(p.dense, v[v != 0])
         assert p.dense.dtype == v.dtype
         np.testing.assert_array_equal(F.unpack(p), v)
+
+
+@pytest.mark.parametrize("n,theta,mode,nm", [(3 * 65536 + 40960, 0.9, "count", (8, 3)), (5001, 0.5, "count", (6, 2)),
+                                             (70_000, 0.7, "energy", (8, 3))])
+def test_spectrum_error_parseval(n, theta, mode, nm):
+    """fgc_spectrum_error: the sender-side Parseval error equals the
+    time-domain ||x - decompress(compress(x))||^2 and ||x||^2 (float64)."""
+    from paper_1811_08596_b200 import _lib, _device as D
+    rng = np.random.default_rng(n)
+    g = rng.standard_normal(n) * 1e-2
+    q = F.calibrate([g], *nm)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta, mode), q)
+    msg = F.compress(g, cfg)
+    plan, dm = msg.device_message()
+    spec = torch.from_numpy(debug.forward_spectrum(g, cfg).view(np.float32).reshape(-1, 2).copy()).cuda()
+    en = torch.empty((plan.n_chunks, 2), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib.fgc_spectrum_error(plan.handle, spec.data_ptr(), dm.data_ptr(), en.data_ptr(), D.stream()))
+    err, nrm = en.sum(dim=0).cpu().numpy()
+    rec = F.decompress(msg)
+    assert err == pytest.approx(float(np.sum((g - rec) ** 2)), rel=1e-5)
+    assert nrm == pytest.approx(float(np.sum(g * g)), rel=1e-5)
