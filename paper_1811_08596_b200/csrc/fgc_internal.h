@@ -245,6 +245,8 @@ fgc_status exchange_publish_event(fgc_exchange* x, int k, uint64_t lo, uint64_t 
                                   uint32_t value, int fi = -1);
 fgc_status exchange_publish_piece(fgc_exchange* x, int k, uint32_t i, uint64_t lo, uint64_t bytes,
                                   uint32_t count_target, uint32_t value);
+fgc_status exchange_publish_used(fgc_exchange* x, int k, const ChunkInfo* d_chunks, uint32_t n_chunks, int n_bits,
+                                 cudaEvent_t ready, uint32_t value, int fi = -1);
 fgc_status exchange_wait(fgc_exchange* x, cudaStream_t s, int fi, uint32_t value);
 PieceCounter exchange_counter(fgc_exchange* x, uint32_t first, uint32_t per);
 PieceWait exchange_piece_wait(fgc_exchange* x, uint32_t first, uint32_t per, uint32_t target);

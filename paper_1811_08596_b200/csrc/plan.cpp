@@ -874,7 +874,8 @@ static fgc_status exchange_average_impl(fgc_plan* p, fgc_exchange* x, const void
     // energy mode: no fused chunks; the whole message is one piece
     FGC_TRY(energy_compress(p, grad, dtype, nullptr, message, nullptr, flags, s));
     FGC_CUDA(cudaEventRecord(ev_tail, s));
-    FGC_TRY(exchange_publish_event(x, k, 0, p->msg_bytes, ev_tail, tval));
+    // energy messages are sized for every slot: push each segment's used bytes only
+    FGC_TRY(exchange_publish_used(x, k, p->d_chunks, p->n_chunks, p->q.n_bits, ev_tail, tval));
     FGC_TRY(exchange_wait(x, s, (int)Pmax, tval));
     FGC_TRY(decode_range(p, gathered, W, p->msg_bytes, w, out, s, p->fused_first, p->fused_count, true));
     FGC_TRY(exchange_join(x, s));
@@ -1046,7 +1047,10 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
     else FGC_TRY(compress_range(p, dev_grad, dtype, message, flags, g, 0, 0, true));
     if (x) {
       FGC_CUDA(cudaEventRecord(p->ev_c2[P], g));
-      FGC_TRY(exchange_publish_event(x, k, m_lo, p->msg_bytes - m_lo, p->ev_c2[P], tval, (int)Pmax));
+      if (energy)
+        FGC_TRY(exchange_publish_used(x, k, p->d_chunks, p->n_chunks, p->q.n_bits, p->ev_c2[P], tval, (int)Pmax));
+      else
+        FGC_TRY(exchange_publish_event(x, k, m_lo, p->msg_bytes - m_lo, p->ev_c2[P], tval, (int)Pmax));
       FGC_TRY(exchange_wait(x, g, (int)Pmax, tval));
     }
     FGC_TRY(decode_range(p, gathered, W, p->msg_bytes, w, dev_out, g, energy ? p->fused_first : 0,

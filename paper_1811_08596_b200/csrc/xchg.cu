@@ -81,6 +81,46 @@ __global__ void k_flag_wait(const uint32_t* flags, int nranks, int me, uint32_t 
   }
 }
 
+// Variable-length push (energy mode): every chunk segment of this rank's
+// message is copied to every peer only up to its used bytes -- the header,
+// the bitmap and the codes the segment's own nnz says it holds (rounded to 16
+// bytes, what the decode reads) -- instead of the full-capacity segment.  The
+// sizes live on the device, so SMs copy (one CTA per chunk, 16-byte stores
+// into the peers' IPC-mapped buffers); the last CTA to finish sets the flag
+// in every peer after a system-scope fence.
+struct PushPeers {
+  uint8_t* dst[kMaxRanks];             // the peer's copy of this rank's slot
+  uint32_t* flag[kMaxRanks];           // this rank's flag for the piece in the peer
+  int n;
+};
+
+__global__ void k_push_used(const fgc::ChunkInfo* chunks, uint32_t n_chunks, const uint8_t* src, int N, PushPeers pp,
+                            uint32_t value, uint32_t* done, unsigned long long* pushed) {
+  const fgc::ChunkInfo ci = chunks[blockIdx.x];
+  const uint8_t* seg = src + ci.seg_off;
+  const uint32_t nnz = *reinterpret_cast<const uint32_t*>(seg);
+  const uint64_t code_bytes = 16ull * (((uint64_t)nnz * (uint32_t)N + 127u) / 128u);
+  const uint64_t cap = ci.code_off + 4ull * ((ci.code_cap + 3u) & ~3u);
+  const uint64_t bytes = min((uint64_t)ci.code_off + code_bytes, cap);
+  const uint4* s4 = reinterpret_cast<const uint4*>(seg);
+  const uint32_t n4 = (uint32_t)(bytes / 16);
+  for (int p = 0; p < pp.n; ++p) {
+    uint4* d4 = reinterpret_cast<uint4*>(pp.dst[p] + ci.seg_off);
+    for (uint32_t e = threadIdx.x; e < n4; e += blockDim.x) d4[e] = s4[e];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(pushed, (unsigned long long)bytes * pp.n);
+    if (atomicAdd(done, 1u) == n_chunks - 1) {
+      __threadfence_system();
+      for (int p = 0; p < pp.n; ++p)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pp.flag[p]), "r"(value) : "memory");
+      *done = 0u;                                       // ready for the next step's launch
+    }
+  }
+}
+
 }  // namespace
 
 struct fgc_exchange {
@@ -89,6 +129,8 @@ struct fgc_exchange {
   uint8_t* gbuf = nullptr;            // 2 * nranks * msg_bytes (buffer k at k * nranks * msg_bytes)
   uint32_t* flags = nullptr;          // [kMaxRanks][kFlagStride] step counters written by the peers
   uint32_t* pcnt = nullptr;           // [kMaxPieces] completed chunks per piece (this rank's compress)
+  uint32_t* push_done = nullptr;      // k_push_used: finished chunk CTAs of the running launch
+  unsigned long long* pushed = nullptr;   // bytes pushed by k_push_used (diagnostics)
   uint8_t* peer_gbuf[kMaxRanks] = {};
   uint32_t* peer_flags[kMaxRanks] = {};
   cudaStream_t cs[2][kCopyStreams] = {};
@@ -127,6 +169,9 @@ extern "C" fgc_status fgc_exchange_create(int nranks, int rank, uint64_t message
   if (e == cudaSuccess) e = cudaMemset(x->flags, 0, sizeof(uint32_t) * kMaxRanks * kFlagStride);
   if (e == cudaSuccess) e = cudaMalloc(&x->pcnt, sizeof(uint32_t) * kMaxPieces);
   if (e == cudaSuccess) e = cudaMemset(x->pcnt, 0, sizeof(uint32_t) * kMaxPieces);
+  if (e == cudaSuccess) e = cudaMalloc(&x->push_done, sizeof(uint32_t) + sizeof(unsigned long long) * 2);
+  if (e == cudaSuccess) e = cudaMemset(x->push_done, 0, sizeof(uint32_t) + sizeof(unsigned long long) * 2);
+  if (e == cudaSuccess) x->pushed = reinterpret_cast<unsigned long long*>(x->push_done + 2);
   if (e == cudaSuccess) e = cudaMemset(x->gbuf, 0, 2ull * nranks * message_bytes);
   for (int c = 0; c < 2; ++c)
     for (int i = 0; i < kCopyStreams && e == cudaSuccess; ++i)
@@ -190,6 +235,7 @@ extern "C" void fgc_exchange_destroy(fgc_exchange* x) {
   cudaFree(x->gbuf);
   cudaFree(x->flags);
   cudaFree(x->pcnt);
+  cudaFree(x->push_done);
   delete x;
 }
 
@@ -256,6 +302,29 @@ fgc_status exchange_publish_event(fgc_exchange* x, int k, uint64_t lo, uint64_t 
   cudaStream_t cs = x->cs[1][fi % kCopyStreams];
   XC(cudaStreamWaitEvent(cs, ready, 0));
   return push(x, cs, k, lo, bytes, fi, value);
+}
+
+// Variable-length publish of the whole message (energy mode) after `ready`:
+// k_push_used on a copy stream, flag `fi` (default: the generic-chunk slot).
+fgc_status exchange_publish_used(fgc_exchange* x, int k, const ChunkInfo* d_chunks, uint32_t n_chunks, int n_bits,
+                                 cudaEvent_t ready, uint32_t value, int fi) {
+  if (fi < 0) fi = kMaxPieces;
+  cudaStream_t cs = x->cs[1][fi % kCopyStreams];
+  XC(cudaStreamWaitEvent(cs, ready, 0));
+  PushPeers pp{};
+  const uint64_t off = (uint64_t)k * x->nranks * x->msg_bytes + (uint64_t)x->rank * x->msg_bytes;
+  for (int a = 0; a < x->nranks; ++a) {
+    if (a == x->rank) continue;
+    pp.dst[pp.n] = x->peer_gbuf[a] + off;
+    pp.flag[pp.n] = x->peer_flags[a] + x->rank * kFlagStride + fi;
+    ++pp.n;
+  }
+  if (!pp.n) return FGC_OK;
+  k_push_used<<<n_chunks, 256, 0, cs>>>(d_chunks, n_chunks, x->gbuf + off, n_bits, pp, value, x->push_done,
+                                        x->pushed);
+  FGC_LAUNCHED(1);
+  exchange_trace(cs, "used-pushed");
+  return FGC_OK;
 }
 
 // Fused piece i: the copy stream waits (stream memory operation) until the
@@ -377,4 +446,10 @@ extern "C" int fgc_debug_exchange_trace(char* out, int cap) {
   memcpy(out, r.data(), n);
   out[n] = 0;
   return n;
+}
+
+extern "C" unsigned long long fgc_debug_exchange_pushed(fgc_exchange* x) {
+  unsigned long long v = 0;
+  if (x && x->pushed) cudaMemcpy(&v, x->pushed, sizeof(v), cudaMemcpyDeviceToHost);
+  return v;
 }

@@ -57,6 +57,15 @@ def _worker(rank, world, port, n, transport, mode, out_q, theta=0.9, nm=(8, 3), 
             hout = avg.step_host(torch.from_numpy(rows[s][rank]).pin_memory(), theta=thetas[s])
             assert torch.equal(hout, outs[s].cpu()), "host step disagrees"
         avg.check()
+        if transport == "peer" and mode == "energy" and avg.exchange is not None:
+            # energy messages are sized for every slot; only the used bytes travel
+            import ctypes
+            from paper_1811_08596_b200 import _lib
+            f = _lib.lib.fgc_debug_exchange_pushed
+            f.restype, f.argtypes = ctypes.c_ulonglong, [ctypes.c_void_p]
+            pushed = f(avg.exchange.handle)
+            full = (steps + 2) * avg.plan.message_bytes * (world - 1)
+            assert 0 < pushed < full, (pushed, full)
         avg.close()
         # oracle: decode every rank's message of every step (the wire bytes of a
         # rank's compress are bit-identical on all ranks, so serialize locally)
