@@ -394,7 +394,11 @@ def run_ours(args, wl, rank, world, local_rank):
                    "peak_gbs": 900.0, "peak_kind": "nominal per direction per GPU",
                    "frac": (world - 1) * M / (ms * 1e-3) / 1e9 / 900.0,
                    "measured_peer_copy_gbs": 770.0,
-                   "note": "allgather receive (W-1)*M per rank over the step time"},
+                   "exchange": {"1": "direct peer reads", "2": "kernel pushes"}.get(
+                       os.environ.get("FGC_EXCHANGE_DIRECT", "0")[:1], "copy-engine pushes")
+                       if transport == "peer" else transport,
+                   "note": "allgather receive (W-1)*M per rank over the step time (capacity bytes: an upper "
+                           "bound under direct peer reads, which fetch each segment's used bytes only)"},
         "message_bytes": M, "compression_ratio": 4.0 * n / M,
         "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,

@@ -18,6 +18,7 @@ CPU (tests/test_comm_cpu.py).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -53,14 +54,16 @@ def shard_weights(batch_size: int, workers: int) -> np.ndarray:
 
 def config_fingerprint(n: int, config: CodecConfig, capacity_theta: float | None, weights) -> tuple:
     """What every rank of one averaging group must agree on: length, chunk,
-    capacity theta (the message layout), mode, half pass, quantizer lattice
-    and the shard weights."""
+    capacity theta (the message layout), mode, half pass, quantizer lattice,
+    the shard weights and the peer-exchange transport (FGC_EXCHANGE_DIRECT:
+    direct peer reads vs copy-engine pushes wait on different signals)."""
     q = config.quantizer
     spec = config.sparsification
     cap = spec.theta if capacity_theta is None else float(capacity_theta)
     return (int(n), int(config.chunk_size), cap, spec.mode, bool(config.half_precision_pass),
             None if q is None else (q.min, q.max, q.n_bits, q.mantissa_bits, q.eps),
-            tuple(float(x) for x in np.asarray(weights, dtype=np.float64).reshape(-1)))
+            tuple(float(x) for x in np.asarray(weights, dtype=np.float64).reshape(-1)),
+            os.environ.get("FGC_EXCHANGE_DIRECT", "0")[:1] or "0")
 
 
 def check_config_agreement(fingerprint: tuple, group=None, world: int | None = None) -> None:

@@ -102,6 +102,15 @@ __device__ __forceinline__ uint32_t read_bits(const uint32_t* words, uint64_t po
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// A chunk's completion tag: system scope when peers on other GPUs read it.
+__device__ __forceinline__ void release_tag(uint32_t* p, uint32_t v, uint32_t sys) {
+  if (sys) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  } else {
+    st_release_gpu(p, v);
+  }
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;

@@ -145,6 +145,13 @@ struct PieceCounter {
   uint32_t first = 0, per = 1;
   uint32_t* done = nullptr;           // per chunk id: set to `tag` (release) once the segment is written
   uint32_t tag = 0;
+  uint32_t sys = 0;                   // release `done` at system scope (peers on other GPUs read it)
+  // kernel pushes (exchange_kpush): CTA r of chunk c's cluster stores its half
+  // of the segment at pdst[p] + seg_off and then releases ptag[p][2c + r] =
+  // pval (system scope) for each of the npeers peers
+  uint8_t* const* pdst = nullptr;
+  uint32_t* const* ptag = nullptr;
+  uint32_t npeers = 0, pval = 0;
 };
 
 // Decode-side wait of the peer exchange: before reading chunk c, every peer
@@ -157,6 +164,13 @@ struct PieceWait {
   // step runs concurrently; the decode is launched as its programmatic dependent)
   const uint32_t* done = nullptr;
   uint32_t tag = 0;
+  // in-kernel transports: before reading chunk c, dtab[b][c * tstride + j]
+  // >= target for every peer b != me and j < tstride (tags its compress
+  // kernel released); message w starts at mtab[w] when set (direct reads of
+  // the peers' own buffers), else in the local gathered stack
+  const uint8_t* const* mtab = nullptr;
+  const uint32_t* const* dtab = nullptr;
+  uint32_t tstride = 1;
 };
 
 // drop_mask (may be null): 1 byte per bin of the chunk-major spectrum; when
@@ -233,6 +247,15 @@ fgc_status launch_compress4(const float2* thi, const float2* tlo, uint32_t ahead
                             uint32_t first, uint32_t count, const void* grad, int dtype, int half_pass,
                             const QuantParams& q, uint8_t* message, uint32_t* flags, float2* fb_spec, float2* dbg,
                             cudaStream_t s, PieceCounter pc);
+// 2-CTA-cluster compress with 1024 threads per CTA (fused_w.cu): the
+// radix-32 columns split over lane pairs; t1024 is W_1024^m.
+fgc_status launch_compress_w(const float2* thi, const float2* tlo, const float2* t1024, uint32_t ahead,
+                             const ChunkInfo* d_chunks, uint32_t first, uint32_t count, const void* grad, int dtype,
+                             int half_pass, const QuantParams& q, uint8_t* message, uint32_t* flags, float2* fb_spec,
+                             float2* dbg, cudaStream_t s, PieceCounter pc);
+// Instrumentation knobs (fgc_debug_set_fused_knobs) and the per-CTA phase
+// timestamp buffer, for fused kernels outside fused.cu (knobs 0: none).
+void fused_debug_state(uint32_t& knobs, unsigned long long*& ts);
 // Debug hooks: the fused kernels' own forward coefficients / inverse.
 fgc_status launch_fused_spectrum(const FusedTables* t, const ChunkInfo* d_chunks, uint32_t first, uint32_t count,
                                  const void* grad, int dtype, int half_pass, float2* spectrum, uint32_t* flags,
@@ -250,6 +273,14 @@ fgc_status exchange_publish_used(fgc_exchange* x, int k, const ChunkInfo* d_chun
 fgc_status exchange_wait(fgc_exchange* x, cudaStream_t s, int fi, uint32_t value);
 PieceCounter exchange_counter(fgc_exchange* x, uint32_t first, uint32_t per);
 PieceWait exchange_piece_wait(fgc_exchange* x, uint32_t first, uint32_t per, uint32_t target);
+// Transport of the fused chunks (FGC_EXCHANGE_DIRECT): 0 copy-engine pushes
+// in pieces (default), 1 direct reads -- the decode reads every peer's
+// segments in the peer's own buffer over NVLink, 2 kernel pushes -- the
+// compress kernel stores each finished segment into the peers' buffers.
+// Both in-kernel transports signal per chunk.
+int exchange_transport(const fgc_exchange* x, uint32_t chunk_end);
+void exchange_direct(fgc_exchange* x, int k, uint32_t tag, PieceCounter& pc, PieceWait& pw);
+void exchange_kpush(fgc_exchange* x, int k, uint32_t tag, PieceCounter& pc, PieceWait& pw);
 uint32_t exchange_max_pieces();
 uint32_t exchange_piece_target(fgc_exchange* x, uint32_t i, uint32_t chunks);
 fgc_status exchange_join(fgc_exchange* x, cudaStream_t s);

@@ -279,6 +279,33 @@ __device__ __noinline__ void resolve_candidates(CompressShared& sh, uint32_t m, 
   }
 }
 
+// Kernel pushes (exchange transport 2): store part `part` of `nparts` of
+// chunk c's finished segment -- header, bitmap and the codes its nnz says it
+// holds, rounded to 16 bytes (what the decode reads) -- into every peer's
+// gather buffer, then release the part's tag(s) there at system scope.
+__device__ __noinline__ void push_parts(PieceCounter pc, const ChunkInfo ci, const uint8_t* message, uint32_t chunk,
+                                        uint32_t N, uint32_t part, uint32_t nparts) {
+  const uint8_t* seg = message + ci.seg_off;
+  const uint32_t nnz = __ldcg(reinterpret_cast<const uint32_t*>(seg));
+  const uint64_t code_bytes = 16ull * (((uint64_t)nnz * N + 127u) / 128u);
+  const uint64_t cap = ci.code_off + 4ull * ((ci.code_cap + 3u) & ~3u);
+  const uint32_t n4 = (uint32_t)(min((uint64_t)ci.code_off + code_bytes, cap) / 16u);
+  const uint32_t lo = part * n4 / nparts, hi = (part + 1) * n4 / nparts;
+  const uint4* s4 = reinterpret_cast<const uint4*>(seg);
+  for (uint32_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+    const uint4 v = __ldcg(s4 + e);
+    for (uint32_t p = 0; p < pc.npeers; ++p) reinterpret_cast<uint4*>(pc.pdst[p] + ci.seg_off)[e] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t p = 0; p < pc.npeers; ++p)
+      for (uint32_t j = part; j < part + (nparts == 1 ? 2u : 1u); ++j)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pc.ptag[p] + 2ull * chunk + j), "r"(pc.pval)
+                     : "memory");
+  }
+}
+
 __device__ __forceinline__ void zero_buf(CompressShared& sh, uint32_t words4) {
   uint4* z = reinterpret_cast<uint4*>(sh.buf);
   for (uint32_t e = threadIdx.x; e < words4; e += kThreads) z[e] = make_uint4(0, 0, 0, 0);
@@ -553,8 +580,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       __syncthreads();
       if (tid == 0) {
         if (a.pc.cnt) atomicAdd(&a.pc.cnt[(chunk - a.pc.first) / a.pc.per], 1u);
-        if (a.pc.done) st_release_gpu(a.pc.done + chunk, a.pc.tag);
+        if (a.pc.done) release_tag(a.pc.done + chunk, a.pc.tag, a.pc.sys);
       }
+      if (a.pc.npeers) push_parts(a.pc, ci, a.message, chunk, (uint32_t)q.n_bits, 0, 1);
     }
     return;
   }
@@ -778,8 +806,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     cluster.sync();                               // (G) every thread of both CTAs has fenced
     if (r == 0 && tid == 0) {
       if (a.pc.cnt) atomicAdd(&a.pc.cnt[(chunk - a.pc.first) / a.pc.per], 1u);
-      if (a.pc.done) st_release_gpu(a.pc.done + chunk, a.pc.tag);
+      if (a.pc.done) release_tag(a.pc.done + chunk, a.pc.tag, a.pc.sys);
     }
+    if (a.pc.npeers) push_parts(a.pc, ci, a.message, chunk, (uint32_t)N, r, 2);
   } else if (fold) {
     cluster.sync();                               // G: CTA 0 finished reading CTA 1's staging
   } else {
@@ -906,7 +935,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     }
     __syncthreads();
   }
-  if (a.pw.flags) {
+  if (a.pw.dtab) {
+    // in-kernel transports: every peer's compress kernel has released this
+    // chunk (direct reads: its own tag, remote; kernel pushes: both CTAs'
+    // tags, local, set after their stores into our gather buffer)
+    const uint32_t ts = a.pw.tstride;
+    if (tid < (uint32_t)a.pw.nranks * ts && (int)(tid / ts) != a.pw.me) {
+      const uint32_t* f = a.pw.dtab[tid / ts] + chunk * ts + tid % ts;
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if ((int32_t)(v - a.pw.target) >= 0) break;
+        __nanosleep(128);
+      }
+    }
+    __syncthreads();
+  } else if (a.pw.flags) {
     // peer exchange: every peer's copy of this chunk's piece has landed
     if (tid < (uint32_t)a.pw.nranks && (int)tid != a.pw.me) {
       const uint32_t* f = a.pw.flags + tid * a.pw.stride + (chunk - a.pw.first) / a.pw.per;
@@ -919,7 +963,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     }
     __syncthreads();
   }
-  if (!a.spectrum && tid < (uint32_t)a.W && blockIdx.x / 2 + a.ahead < a.count) {
+  // message w of the step: a peer's own buffer (direct reads) or the gathered stack
+  auto mbase = [&](int w) -> const uint8_t* {
+    return a.pw.mtab ? a.pw.mtab[w] : a.messages + (uint64_t)w * a.stride;
+  };
+  if (!a.spectrum && tid < (uint32_t)a.W && blockIdx.x / 2 + a.ahead < a.count && !(dbg & 8u) &&
+      (!a.pw.mtab || (int)tid == a.pw.me)) {
     // message segments of the chunk the next wave decodes here (CTA r: half of each)
     const ChunkInfo cn = a.chunks[chunk + a.ahead];
     const uint32_t seg = (uint32_t)(cn.code_off + 4ull * ((cn.code_cap + 3u) & ~3u));
@@ -927,7 +976,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     const uint32_t lo = r ? half : 0u, bytes = r ? seg - half : half;
     if (bytes)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                   ::"l"(a.messages + (uint64_t)tid * a.stride + cn.seg_off + lo), "r"(bytes) : "memory");
+                   ::"l"(mbase((int)tid) + cn.seg_off + lo), "r"(bytes) : "memory");
   }
 
   if (a.spectrum) {
@@ -956,7 +1005,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           soff[i] = ~0u;
           if (tid == 0) sh.soff[i] = ~0u;
           if (i < G) {
-            const uint8_t* sg = a.messages + (uint64_t)(w0 + i) * a.stride + ci.seg_off;
+            const uint8_t* sg = mbase(w0 + i) + ci.seg_off;
             const uint32_t nnz = __ldg(reinterpret_cast<const uint32_t*>(sg));
             const uint32_t used4 = (uint32_t)min((((uint64_t)nnz * N + 127u) >> 7), (uint64_t)((ci.code_cap + 3u) >> 2));
             FGC_CHECK(nnz <= 2u * ci.bins);
@@ -975,7 +1024,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         cnt2[i][0] = cnt2[i][1] = 0u;
         if (i < G) {
           const uint32_t* bmg =
-              reinterpret_cast<const uint32_t*>(a.messages + (uint64_t)(w0 + i) * a.stride + ci.seg_off + kSegHeader);
+              reinterpret_cast<const uint32_t*>(mbase(w0 + i) + ci.seg_off + kSegHeader);
           const uint4 q4 = __ldg(reinterpret_cast<const uint4*>(bmg) + tid);
           const uint4 nat = make_uint4(ballot_to_wire(q4.x), ballot_to_wire(q4.y), ballot_to_wire(q4.z),
                                        ballot_to_wire(q4.w));
@@ -1066,8 +1115,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
             walk(m2, nf);
           } else {
             // codes from global memory through a 4-word register window
-            const uint32_t* cw = reinterpret_cast<const uint32_t*>(a.messages + (uint64_t)(w0 + i) * a.stride +
-                                                                   ci.seg_off + ci.code_off);
+            const uint32_t* cw = reinterpret_cast<const uint32_t*>(mbase(w0 + i) + ci.seg_off + ci.code_off);
             const uint32_t wb = (k * N) >> 5;
             uint32_t A = wb < ci.code_cap ? __ldg(cw + wb) : 0u;
             uint32_t B = wb + 1 < ci.code_cap ? __ldg(cw + wb + 1) : 0u;
@@ -1196,10 +1244,20 @@ fgc_status set_smem(K kernel, size_t bytes) {
 
 bool fused_available() { return true; }
 
+static uint32_t g_fused_dbg_host = 0;
+// the knobs and timestamp buffer for kernels in other translation units
+void fused_debug_state(uint32_t& knobs, unsigned long long*& ts) {
+  knobs = g_fused_dbg_host;
+  void* p = nullptr;
+  ts = (knobs && cudaGetSymbolAddress(&p, g_fused_ts) == cudaSuccess) ? static_cast<unsigned long long*>(p) : nullptr;
+  if (!ts) knobs = 0;
+}
+
 }  // namespace fgc
 
 // Internal instrumentation hooks (not part of the public header).
 extern "C" int fgc_debug_set_fused_knobs(uint32_t knobs) {
+  fgc::g_fused_dbg_host = knobs;
   return cudaMemcpyToSymbol(fgc::g_fused_dbg, &knobs, sizeof(knobs)) == cudaSuccess ? 0 : 1;
 }
 extern "C" int fgc_debug_set_compress_kernel(int k);
@@ -1262,7 +1320,7 @@ static int g_compress_kernel = -1;
 static int compress_kernel() {
   if (g_compress_kernel < 0) {
     const char* e = getenv("FGC_COMPRESS_KERNEL");
-    g_compress_kernel = (e && e[0] == '4') ? 4 : 2;
+    g_compress_kernel = (e && e[0] == '4') ? 4 : (e && e[0] == '1') ? 1 : 2;
   }
   return g_compress_kernel;
 }
@@ -1272,9 +1330,13 @@ static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_
                                        const QuantParams& q, uint8_t* message, uint32_t* flags,
                                        float2* fb_spec, float2* dbg, cudaStream_t s, PieceCounter pc) {
   if (!count) return FGC_OK;
-  if (compress_kernel() == 4)
+  // (the alternative kernels do not implement the kernel-push transport)
+  if (compress_kernel() == 4 && !pc.npeers)
     return launch_compress4(t->thi, t->tlo, t->wave, d_chunks, first, count, grad, dtype, half_pass, q, message,
                             flags, fb_spec, dbg, s, pc);
+  if (compress_kernel() == 1 && !pc.npeers)
+    return launch_compress_w(t->thi, t->tlo, t->t1024, t->wave, d_chunks, first, count, grad, dtype, half_pass, q,
+                             message, flags, fb_spec, dbg, s, pc);
   CompressArgs a{d_chunks, first, grad, q, message, flags, t->thi, t->tlo, t->t1024, fb_spec, dbg, count, t->wave,
                  pc};
   const size_t smem = sizeof(CompressShared);
@@ -1361,6 +1423,6 @@ fgc_status launch_fused_inverse(const FusedTables* t, const ChunkInfo* d_chunks,
 }  // namespace fgc
 
 extern "C" int fgc_debug_set_compress_kernel(int k) {
-  fgc::g_compress_kernel = (k == 4) ? 4 : 2;
+  fgc::g_compress_kernel = (k == 4 || k == 1) ? k : 2;
   return 0;
 }

@@ -611,7 +611,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kT, 2) k_fused_compr
       __syncthreads();
       if (tid == 0) {
         if (a.pc.cnt) atomicAdd(&a.pc.cnt[(chunk - a.pc.first) / a.pc.per], 1u);
-        if (a.pc.done) st_release_gpu(a.pc.done + chunk, a.pc.tag);
+        if (a.pc.done) release_tag(a.pc.done + chunk, a.pc.tag, a.pc.sys);
       }
     }
     return;
@@ -823,7 +823,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(kT, 2) k_fused_compr
     cluster.sync();                               // (G) every thread of the cluster has fenced
     if (r == 0 && tid == 0) {
       if (a.pc.cnt) atomicAdd(&a.pc.cnt[(chunk - a.pc.first) / a.pc.per], 1u);
-      if (a.pc.done) st_release_gpu(a.pc.done + chunk, a.pc.tag);
+      if (a.pc.done) release_tag(a.pc.done + chunk, a.pc.tag, a.pc.sys);
     }
   } else if (fold) {
     cluster.sync();                               // G: owners finished reading the peers' staging

@@ -899,7 +899,32 @@ static fgc_status exchange_average_impl(fgc_plan* p, fgc_exchange* x, const void
     exchange_trace(p->side, "tail-decoded");
     FGC_CUDA(cudaEventRecord(ev_side, p->side));
   }
-  if (p->fused_count) {
+  const int transport = p->fused_count ? exchange_transport(x, p->fused_first + p->fused_count) : 0;
+  if (transport) {
+    // in-kernel transports, signalled per chunk (no copy streams, no pieces):
+    // 1: the compress kernel releases each chunk's tag at system scope and
+    //    the decode (its programmatic dependent) reads every peer's segment
+    //    in the peer's own buffer once the peer's tag is there;
+    // 2: the compress kernel stores each finished segment into every peer's
+    //    gather buffer and releases the chunk's tags there; the decode reads
+    //    the local gather buffer once the peers' tags arrived
+    PieceCounter pc;
+    PieceWait pw;
+    if (transport == 1) {
+      exchange_direct(x, k, tval, pc, pw);
+    } else {
+      exchange_kpush(x, k, tval, pc, pw);
+      pc.done = p->d_done;
+      pc.tag = ++p->tag;
+      pw.done = p->d_done;
+      pw.tag = pc.tag;
+    }
+    FGC_TRY(launch_fused_compress(p->fused, p->d_chunks, p->fused_first, p->fused_count, grad, dtype,
+                                  p->desc.half_pass, p->q, message, flags, p->d_spec, s, pc));
+    FGC_TRY(launch_fused_decode(p->fused, p->d_chunks, p->fused_first, p->fused_count, gathered, W, p->msg_bytes,
+                                w, p->q, out, s, pw));
+    exchange_trace(s, "decoded");
+  } else if (p->fused_count) {
     // one compress launch; the kernel counts finished chunks per piece and the
     // copy streams push each piece the moment its count is complete
     // 4 pieces measured best at N=2 and N=4 (8: +5%, 16: +15%, 1: +20%)

@@ -39,6 +39,16 @@ constexpr int kMaxRanks = 64;
 constexpr int kMaxPieces = 32;                         // fused pieces; flag index kMaxPieces = generic chunks
 constexpr int kFlagStride = kMaxPieces + 1;
 constexpr int kCopyStreams = 4;                        // per publisher class (fused pieces / generic chunks)
+// Per-chunk completion tags of the in-kernel transports, after the flag words
+// in the same (IPC-exported) allocation: region b (nranks regions of
+// 2 * kTagChunks words) holds rank b's tags.
+//   direct reads:  tags_b[c] in rank b's own memory, set once b's compress
+//                  kernel wrote chunk c's segment (the readers poll it remotely)
+//   kernel pushes: tags_b[2c + r] in every receiver's memory, set by CTA r of
+//                  b's compress cluster once it stored its half of the segment
+//                  into the receiver's gather buffer (the receiver polls locally)
+constexpr uint32_t kFlagWords = kMaxRanks * kFlagStride;
+constexpr uint32_t kTagChunks = 1u << 14;
 
 struct MemOps {
   WriteValueFn write = nullptr;
@@ -133,6 +143,13 @@ struct fgc_exchange {
   unsigned long long* pushed = nullptr;   // bytes pushed by k_push_used (diagnostics)
   uint8_t* peer_gbuf[kMaxRanks] = {};
   uint32_t* peer_flags[kMaxRanks] = {};
+  // device tables (filled at open): [0, 2R) where rank b's message of buffer
+  // k lives in b's memory (direct reads); [2R, 3R) rank b's tag region in b's
+  // memory; [3R, 4R) rank b's tag region in this rank's memory; [4R, 6R) this
+  // rank's slot of buffer k in peer p's memory (kernel pushes, peers only);
+  // [6R, 7R) this rank's tag region in peer p's memory (peers only)
+  void** d_tab = nullptr;
+  int xmode = 0;                      // FGC_EXCHANGE_DIRECT: 0 copy-engine pushes, 1 direct reads, 2 kernel pushes
   cudaStream_t cs[2][kCopyStreams] = {};
   std::vector<cudaEvent_t> ev;        // per piece: compress done on the caller's stream
   cudaEvent_t ev_copies = nullptr;
@@ -165,8 +182,11 @@ extern "C" fgc_status fgc_exchange_create(int nranks, int rank, uint64_t message
   x->rank = rank;
   x->msg_bytes = message_bytes;
   cudaError_t e = cudaMalloc(&x->gbuf, 2ull * nranks * message_bytes);
-  if (e == cudaSuccess) e = cudaMalloc(&x->flags, sizeof(uint32_t) * kMaxRanks * kFlagStride);
-  if (e == cudaSuccess) e = cudaMemset(x->flags, 0, sizeof(uint32_t) * kMaxRanks * kFlagStride);
+  const size_t fwords = kFlagWords + (size_t)nranks * 2 * kTagChunks;
+  if (e == cudaSuccess) e = cudaMalloc(&x->flags, sizeof(uint32_t) * fwords);
+  if (e == cudaSuccess) e = cudaMemset(x->flags, 0, sizeof(uint32_t) * fwords);
+  if (e == cudaSuccess) e = cudaMalloc(&x->d_tab, sizeof(void*) * 7 * kMaxRanks);
+  if (const char* d = getenv("FGC_EXCHANGE_DIRECT")) x->xmode = (d[0] == '1') ? 1 : (d[0] == '2') ? 2 : 0;
   if (e == cudaSuccess) e = cudaMalloc(&x->pcnt, sizeof(uint32_t) * kMaxPieces);
   if (e == cudaSuccess) e = cudaMemset(x->pcnt, 0, sizeof(uint32_t) * kMaxPieces);
   if (e == cudaSuccess) e = cudaMalloc(&x->push_done, sizeof(uint32_t) + sizeof(unsigned long long) * 2);
@@ -215,6 +235,27 @@ extern "C" fgc_status fgc_exchange_open(fgc_exchange* x, const uint8_t* all_hand
     x->peer_gbuf[a] = static_cast<uint8_t*>(pg);
     x->peer_flags[a] = static_cast<uint32_t*>(pf);
   }
+  // tables of the in-kernel transports (rank b compresses buffer k's message
+  // into its own slot b of its own buffer k)
+  const int R = kMaxRanks;
+  const void* tab[7 * kMaxRanks] = {};
+  const uint64_t treg = 2ull * kTagChunks;
+  for (int k = 0; k < 2; ++k)
+    for (int b = 0; b < x->nranks; ++b)
+      tab[k * R + b] = x->peer_gbuf[b] + ((uint64_t)k * x->nranks + b) * x->msg_bytes;
+  for (int b = 0; b < x->nranks; ++b) {
+    tab[2 * R + b] = x->peer_flags[b] + kFlagWords + b * treg;
+    tab[3 * R + b] = x->flags + kFlagWords + b * treg;
+  }
+  int np = 0;
+  for (int b = 0; b < x->nranks; ++b) {
+    if (b == x->rank) continue;
+    for (int k = 0; k < 2; ++k)
+      tab[4 * R + k * R + np] = x->peer_gbuf[b] + ((uint64_t)k * x->nranks + x->rank) * x->msg_bytes;
+    tab[6 * R + np] = x->peer_flags[b] + kFlagWords + x->rank * treg;
+    ++np;
+  }
+  XC(cudaMemcpy(x->d_tab, tab, sizeof(tab), cudaMemcpyHostToDevice));
   x->opened = true;
   return FGC_OK;
 }
@@ -236,6 +277,7 @@ extern "C" void fgc_exchange_destroy(fgc_exchange* x) {
   cudaFree(x->flags);
   cudaFree(x->pcnt);
   cudaFree(x->push_done);
+  cudaFree(x->d_tab);
   delete x;
 }
 
@@ -383,6 +425,48 @@ PieceWait exchange_piece_wait(fgc_exchange* x, uint32_t first, uint32_t per, uin
   pw.nranks = x->nranks;
   pw.me = x->rank;
   return pw;
+}
+
+int exchange_transport(const fgc_exchange* x, uint32_t chunk_end) {
+  return (x->nranks > 1 && chunk_end <= kTagChunks) ? x->xmode : 0;
+}
+
+// Direct reads: the compress kernel releases tags_me[c] in this rank's own
+// memory at system scope; the decode reads message b from mtab[b] once
+// rank b's tags_b[c] (remote) reached the step's tag.
+void exchange_direct(fgc_exchange* x, int k, uint32_t tag, PieceCounter& pc, PieceWait& pw) {
+  const int R = kMaxRanks;
+  pc = PieceCounter();
+  pc.done = x->flags + kFlagWords + (uint64_t)x->rank * 2 * kTagChunks;
+  pc.tag = tag;
+  pc.sys = 1;
+  pw = PieceWait();
+  pw.nranks = x->nranks;
+  pw.me = x->rank;
+  pw.target = tag;
+  pw.done = pc.done;                  // own chunk: released by the compress grid this decode depends on
+  pw.tag = tag;
+  pw.mtab = reinterpret_cast<const uint8_t* const*>(x->d_tab + (k & 1) * R);
+  pw.dtab = reinterpret_cast<const uint32_t* const*>(x->d_tab + 2 * R);
+  pw.tstride = 1;
+}
+
+// Kernel pushes: each CTA of the compress cluster stores its half of the
+// chunk's segment into every peer's gather buffer and releases tags_me[2c+r]
+// there; the decode reads the local gather buffer once every peer's two tags
+// of the chunk (local memory) reached the step's tag.  The caller sets the
+// own-chunk done/tag pair (the decode's programmatic-dependency wait).
+void exchange_kpush(fgc_exchange* x, int k, uint32_t tag, PieceCounter& pc, PieceWait& pw) {
+  const int R = kMaxRanks;
+  pc.pdst = reinterpret_cast<uint8_t* const*>(x->d_tab + 4 * R + (k & 1) * R);
+  pc.ptag = reinterpret_cast<uint32_t* const*>(x->d_tab + 6 * R);
+  pc.npeers = (uint32_t)(x->nranks - 1);
+  pc.pval = tag;
+  pw.nranks = x->nranks;
+  pw.me = x->rank;
+  pw.target = tag;
+  pw.dtab = reinterpret_cast<const uint32_t* const*>(x->d_tab + 3 * R);
+  pw.tstride = 2;
 }
 
 uint32_t exchange_max_pieces() { return kMaxPieces; }

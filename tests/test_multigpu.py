@@ -32,6 +32,11 @@ def _worker(rank, world, port, n, transport, mode, out_q, theta=0.9, nm=(8, 3), 
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    # "peer": copy-engine pushes into a local gather buffer; "peer-direct":
+    # the decode reads the peers' fused segments in place over NVLink;
+    # "peer-kpush": the compress kernel stores its segments into the peers'
+    os.environ["FGC_EXCHANGE_DIRECT"] = {"peer-direct": "1", "peer-kpush": "2"}.get(transport, "0")
+    transport = "peer" if transport.startswith("peer") else transport
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -86,8 +91,9 @@ def _worker(rank, world, port, n, transport, mode, out_q, theta=0.9, nm=(8, 3), 
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("transport,mode", [("peer", "count"), ("nccl", "count"), ("peer", "energy"),
-                                            ("nccl", "energy")])
+@pytest.mark.parametrize("transport,mode", [("peer", "count"), ("peer-direct", "count"), ("peer-kpush", "count"),
+                                            ("nccl", "count"),
+                                            ("peer", "energy"), ("nccl", "energy")])
 @pytest.mark.parametrize("n", [3 * 65536 + 40960, 1_000_000])
 def test_compressed_average_two_ranks(n, transport, mode):
     import torch.multiprocessing as mp
@@ -106,8 +112,9 @@ def test_compressed_average_two_ranks(n, transport, mode):
     assert len({d for _, _, d in res}) == 1, "ranks disagree bitwise"
 
 
+@pytest.mark.parametrize("transport", ["peer", "peer-direct", "peer-kpush"])
 @pytest.mark.parametrize("seed", range(4))
-def test_random_configs_two_ranks(seed):
+def test_random_configs_two_ranks(seed, transport):
     """Random sizes, keep ratios and lattices over the peer exchange, with
     degenerate chunks on one rank."""
     import torch.multiprocessing as mp
@@ -120,7 +127,7 @@ def test_random_configs_two_ranks(seed):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, "peer", "count", q, theta, nm, special))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, transport, "count", q, theta, nm, special))
              for r in range(world)]
     for p in procs:
         p.start()

@@ -1,6 +1,7 @@
-"""Quick check of the 4-CTA compress kernel against the 2-CTA one and the oracle.
+"""Quick check of an alternate compress kernel (env ALT: 4 = fused4.cu, 1 =
+fused_w.cu) against the default 2-CTA one and the oracle.
 argv: n theta nbits mbits"""
-import ctypes, sys, time
+import ctypes, os, sys, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np
@@ -19,20 +20,21 @@ g = (torch.randn(n, device="cuda", generator=torch.Generator("cuda").manual_seed
 q = F.calibrate([g[: min(n, 4 * 65536)].double().cpu().numpy()], *nm)
 cfg = F.CodecConfig(F.SparsificationSpec(theta), q)
 res = {}
-for k in (2, 4):
+ALT = int(os.environ.get("ALT", "4"))
+for k in (2, ALT):
     lib.fgc_debug_set_compress_kernel(k)
     spec = debug.forward_spectrum(g, cfg)
     m = F.compress(g, cfg)
     torch.cuda.synchronize()
     res[k] = (spec, debug.message_bytes(m))
-s2, s4 = res[2][0], res[4][0]
+s2, s4 = res[2][0], res[ALT][0]
 err = np.abs(s4.astype(np.complex128) - s2.astype(np.complex128)).max() / np.sqrt(np.mean(np.abs(s2.astype(np.complex128)) ** 2))
-print("spectrum max |4 - 2| / rms:", err)
+print("spectrum max |alt - 2| / rms:", err)
 # oracle encode of the 4-kernel's coefficients
 lat = O.lattice(q.min, q.max, q.n_bits, q.mantissa_bits, q.eps)
 lengths = O.chunk_lengths(n, 65536)
 layout, total = O.device_layout(n, 65536, theta, nm[0])
-buf = res[4][1]
+buf = res[ALT][1]
 pos = 0
 bad = 0
 for c, L in enumerate(lengths):
@@ -48,4 +50,4 @@ for c, L in enumerate(lengths):
         if bad < 4:
             print("chunk", c, "differs: nnz", nnz, ch.codes.size, "bm eq", bm == O.flags_to_bytes(ch.bitmap))
     pos += b
-print("chunks", len(lengths), "differing", bad, "| msg equal to 2-CTA kernel:", res[2][1] == res[4][1])
+print("chunks", len(lengths), "differing", bad, "| msg equal to 2-CTA kernel:", res[2][1] == res[ALT][1])
