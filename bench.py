@@ -374,7 +374,8 @@ def run_ours(args, wl, rank, world, local_rank):
     traffic = None        # DRAM bytes per launch of that kernel from the committed ncu --set full capture
     try:
         tr = json.load(open(Path(__file__).resolve().parent / "profiles" / "traffic.json"))
-        if not args.n and (dom[0] == "compress" or world == 1):
+        default_cfg = not args.n and args.theta_drop is None and args.n_bits is None and args.mbits is None
+        if default_cfg and (dom[0] == "compress" or world == 1):
             traffic = tr.get(args.workload, {}).get(dom[0])
     except (OSError, ValueError):
         pass
@@ -428,6 +429,10 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--mode", default="count", choices=["count", "energy"],
                     help="sparsification rule (spectral.py:124-139); the headline is count mode")
+    ap.add_argument("--theta-drop", type=float, default=None,
+                    help="override the workload's theta (BASELINE config 3 sweeps keep 0.01/0.05/0.1/0.3)")
+    ap.add_argument("--n-bits", type=int, default=None, help="override the range-float width (config 4 sweep)")
+    ap.add_argument("--mbits", type=int, default=None, help="override the mantissa bits (with --n-bits)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default=None, choices=["peer", "nccl"],
                     help="exchange for N>1: peer-to-peer copies (default) or one NCCL allgather")
@@ -435,6 +440,13 @@ def main():
     wl = dict(WORKLOADS[args.workload])
     if args.n:
         wl["n"] = args.n
+    if args.theta_drop is not None:
+        wl["theta"] = args.theta_drop
+    if args.n_bits is not None:
+        wl["n_bits"] = args.n_bits
+        wl["mbits"] = args.mbits if args.mbits is not None else {4: 2, 6: 2, 8: 3, 16: 9}.get(args.n_bits, 3)
+    elif args.mbits is not None:
+        wl["mbits"] = args.mbits
     wl["mode"] = args.mode
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `bench.py --gpus N` outside torchrun: launch the N ranks ourselves
