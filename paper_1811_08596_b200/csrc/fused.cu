@@ -997,41 +997,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       // 1a. every bitmap word of the batch (thread t: blocks 2t, 2t+1), block code prefixes;
       //     the code streams of the messages that fit are staged in smem meanwhile
       uint32_t cnt2[kDecBatch][2];
-      uint32_t soff[kDecBatch];                 // staging offset in words, or ~0u: read from global
       {
+        // Every load of the batch in flight at once: the segment headers
+        // (one latency), then the bitmaps and the staged code streams
+        // together (a second).  Issued message by message, each header load
+        // serialised the next message's loads behind it.
+        const uint8_t* sg[kDecBatch];
+        uint32_t nnz[kDecBatch];
+#pragma unroll
+        for (int i = 0; i < kDecBatch; ++i) {
+          sg[i] = mbase(w0 + min(i, G - 1)) + ci.seg_off;
+          nnz[i] = (i < G) ? __ldg(reinterpret_cast<const uint32_t*>(sg[i])) : 0u;
+        }
+        uint4 q4[kDecBatch];
+        uint32_t qN[kDecBatch];
+#pragma unroll
+        for (int i = 0; i < kDecBatch; ++i) {
+          q4[i] = (i < G) ? __ldg(reinterpret_cast<const uint4*>(sg[i] + kSegHeader) + tid) : make_uint4(0, 0, 0, 0);
+          qN[i] = (i < G && tid == 0) ? __ldg(reinterpret_cast<const uint32_t*>(sg[i] + kSegHeader) + 2 * kThreads * 2)
+                                      : 0u;
+        }
+        // message i's used code words go to stage[off[i], off[i] + s4[i]) (uint4 units) while they fit
+        uint32_t off[kDecBatch], s4[kDecBatch];
         uint32_t used_total = 0;
 #pragma unroll
         for (int i = 0; i < kDecBatch; ++i) {
-          soff[i] = ~0u;
-          if (tid == 0) sh.soff[i] = ~0u;
-          if (i < G) {
-            const uint8_t* sg = mbase(w0 + i) + ci.seg_off;
-            const uint32_t nnz = __ldg(reinterpret_cast<const uint32_t*>(sg));
-            const uint32_t used4 = (uint32_t)min((((uint64_t)nnz * N + 127u) >> 7), (uint64_t)((ci.code_cap + 3u) >> 2));
-            FGC_CHECK(nnz <= 2u * ci.bins);
-            if (!(dbg & 4u) && used_total + 4u * used4 <= kDecStageWords) {
-              soff[i] = used_total;
-              if (tid == 0) sh.soff[i] = used_total;
-              const uint4* src = reinterpret_cast<const uint4*>(sg + ci.code_off);
-              for (uint32_t e = tid; e < used4; e += kThreads) sh.stage[(used_total >> 2) + e] = __ldg(src + e);
-              used_total += 4u * used4;
-            }
+          const uint32_t used4 =
+              (uint32_t)min((((uint64_t)nnz[i] * N + 127u) >> 7), (uint64_t)((ci.code_cap + 3u) >> 2));
+          FGC_CHECK(nnz[i] <= 2u * ci.bins);
+          const bool st = i < G && !(dbg & 4u) && 4u * (used_total + used4) <= kDecStageWords;
+          off[i] = used_total;
+          s4[i] = st ? used4 : 0u;
+          if (tid == 0) sh.soff[i] = st ? 4u * used_total : ~0u;
+          used_total += s4[i];
+        }
+        constexpr int kPer = kDecStageWords / 4 / kThreads;
+        uint4 tmp[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const uint32_t e = tid + u * kThreads;
+          if (e < used_total) {
+            const uint8_t* src = sg[0];       // the message holding staged word e (static indices only)
+            uint32_t o = off[0];
+#pragma unroll
+            for (int j = 1; j < kDecBatch; ++j)
+              if (s4[j] && e >= off[j]) { src = sg[j]; o = off[j]; }
+            tmp[u] = __ldg(reinterpret_cast<const uint4*>(src + ci.code_off) + (e - o));
           }
         }
-      }
 #pragma unroll
-      for (int i = 0; i < kDecBatch; ++i) {
-        cnt2[i][0] = cnt2[i][1] = 0u;
-        if (i < G) {
-          const uint32_t* bmg =
-              reinterpret_cast<const uint32_t*>(mbase(w0 + i) + ci.seg_off + kSegHeader);
-          const uint4 q4 = __ldg(reinterpret_cast<const uint4*>(bmg) + tid);
-          const uint4 nat = make_uint4(ballot_to_wire(q4.x), ballot_to_wire(q4.y), ballot_to_wire(q4.z),
-                                       ballot_to_wire(q4.w));
-          reinterpret_cast<uint4*>(sh.bm[i])[tid] = nat;
-          cnt2[i][0] = __popc(nat.x) + __popc(nat.y);
-          cnt2[i][1] = __popc(nat.z) + __popc(nat.w);
-          if (tid == 0) sh.bmN[i] = ballot_to_wire(__ldg(bmg + 2 * kThreads * 2)) & 3u;
+        for (int u = 0; u < kPer; ++u) {
+          const uint32_t e = tid + u * kThreads;
+          if (e < used_total) sh.stage[e] = tmp[u];
+        }
+#pragma unroll
+        for (int i = 0; i < kDecBatch; ++i) {
+          cnt2[i][0] = cnt2[i][1] = 0u;
+          if (i < G) {
+            const uint4 nat = make_uint4(ballot_to_wire(q4[i].x), ballot_to_wire(q4[i].y), ballot_to_wire(q4[i].z),
+                                         ballot_to_wire(q4[i].w));
+            reinterpret_cast<uint4*>(sh.bm[i])[tid] = nat;
+            cnt2[i][0] = __popc(nat.x) + __popc(nat.y);
+            cnt2[i][1] = __popc(nat.z) + __popc(nat.w);
+            if (tid == 0) sh.bmN[i] = ballot_to_wire(qN[i]) & 3u;
+          }
         }
       }
       uint4 tot;
