@@ -311,7 +311,9 @@ __device__ __forceinline__ void zero_buf(CompressShared& sh, uint32_t words4) {
   for (uint32_t e = threadIdx.x; e < words4; e += kThreads) z[e] = make_uint4(0, 0, 0, 0);
 }
 
-template <class T, bool DEBUG, bool HALF>
+// PUSH: the kernel-push exchange transport (a separate instantiation, so the
+// default kernel carries none of its code: measured 1.5% of compress time)
+template <class T, bool DEBUG, bool HALF, bool PUSH = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused_compress(CompressArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CompressShared& sh = *reinterpret_cast<CompressShared*>(smem_raw);
@@ -582,7 +584,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         if (a.pc.cnt) atomicAdd(&a.pc.cnt[(chunk - a.pc.first) / a.pc.per], 1u);
         if (a.pc.done) release_tag(a.pc.done + chunk, a.pc.tag, a.pc.sys);
       }
-      if (a.pc.npeers) push_parts(a.pc, ci, a.message, chunk, (uint32_t)q.n_bits, 0, 1);
+      if constexpr (PUSH) push_parts(a.pc, ci, a.message, chunk, (uint32_t)q.n_bits, 0, 1);
     }
     return;
   }
@@ -808,7 +810,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
       if (a.pc.cnt) atomicAdd(&a.pc.cnt[(chunk - a.pc.first) / a.pc.per], 1u);
       if (a.pc.done) release_tag(a.pc.done + chunk, a.pc.tag, a.pc.sys);
     }
-    if (a.pc.npeers) push_parts(a.pc, ci, a.message, chunk, (uint32_t)N, r, 2);
+    if constexpr (PUSH) push_parts(a.pc, ci, a.message, chunk, (uint32_t)N, r, 2);
   } else if (fold) {
     cluster.sync();                               // G: CTA 0 finished reading CTA 1's staging
   } else {
@@ -902,6 +904,10 @@ __device__ __forceinline__ void y_group(float2 xk, float2 xMk, float2 xkM, float
   y[3] = cmul(make_float2(-w2.x, -w2.y), csub(zMk, zNk));
 }
 
+// TAGS: the in-kernel exchange transports (per-chunk tag waits, and direct
+// reads of the peers' buffers when pw.mtab is set); the default
+// instantiation carries none of that code (measured 1.5 us of decode time)
+template <bool TAGS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused_decode(DecodeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   DecodeShared& sh = *reinterpret_cast<DecodeShared*>(smem_raw);
@@ -935,7 +941,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
     }
     __syncthreads();
   }
-  if (a.pw.dtab) {
+  if (TAGS && a.pw.dtab) {
     // in-kernel transports: every peer's compress kernel has released this
     // chunk (direct reads: its own tag, remote; kernel pushes: both CTAs'
     // tags, local, set after their stores into our gather buffer)
@@ -965,10 +971,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   }
   // message w of the step: a peer's own buffer (direct reads) or the gathered stack
   auto mbase = [&](int w) -> const uint8_t* {
-    return a.pw.mtab ? a.pw.mtab[w] : a.messages + (uint64_t)w * a.stride;
+    if constexpr (TAGS) {
+      if (a.pw.mtab) return a.pw.mtab[w];
+    }
+    return a.messages + (uint64_t)w * a.stride;
   };
   if (!a.spectrum && tid < (uint32_t)a.W && blockIdx.x / 2 + a.ahead < a.count && !(dbg & 8u) &&
-      (!a.pw.mtab || (int)tid == a.pw.me)) {
+      (!TAGS || !a.pw.mtab || (int)tid == a.pw.me)) {
     // message segments of the chunk the next wave decodes here (CTA r: half of each)
     const ChunkInfo cn = a.chunks[chunk + a.ahead];
     const uint32_t seg = (uint32_t)(cn.code_off + 4ull * ((cn.code_cap + 3u) & ~3u));
@@ -1325,7 +1334,12 @@ fgc_status fused_tables_init(FusedTables** t, cudaStream_t s) {
     FGC_TRY(set_smem(k_fused_compress<double, false, true>, cs));
     FGC_TRY(set_smem(k_fused_compress<float, true, true>, cs));
     FGC_TRY(set_smem(k_fused_compress<double, true, true>, cs));
-    FGC_TRY(set_smem(k_fused_decode, sizeof(DecodeShared)));
+    FGC_TRY(set_smem(k_fused_compress<float, false, false, true>, cs));
+    FGC_TRY(set_smem(k_fused_compress<double, false, false, true>, cs));
+    FGC_TRY(set_smem(k_fused_compress<float, false, true, true>, cs));
+    FGC_TRY(set_smem(k_fused_compress<double, false, true, true>, cs));
+    FGC_TRY(set_smem(k_fused_decode<false>, sizeof(DecodeShared)));
+    FGC_TRY(set_smem(k_fused_decode<true>, sizeof(DecodeShared)));
     attrs = true;
   }
   *t = ft;
@@ -1372,7 +1386,11 @@ static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_
   const dim3 grid(2 * count), block(kThreads);
   const bool f64 = dtype == FGC_DTYPE_F64, h = half_pass != 0;
 #define FGC_LAUNCH_FC(T, D, H) k_fused_compress<T, D, H><<<grid, block, smem, s>>>(a)
-  if (dbg) {
+#define FGC_LAUNCH_FP(T, H) k_fused_compress<T, false, H, true><<<grid, block, smem, s>>>(a)
+  if (pc.npeers && !dbg) {
+    if (f64) { if (h) FGC_LAUNCH_FP(double, true); else FGC_LAUNCH_FP(double, false); }
+    else { if (h) FGC_LAUNCH_FP(float, true); else FGC_LAUNCH_FP(float, false); }
+  } else if (dbg) {
     if (f64) { if (h) FGC_LAUNCH_FC(double, true, true); else FGC_LAUNCH_FC(double, true, false); }
     else { if (h) FGC_LAUNCH_FC(float, true, true); else FGC_LAUNCH_FC(float, true, false); }
   } else {
@@ -1380,6 +1398,7 @@ static fgc_status launch_compress_impl(const FusedTables* t, const ChunkInfo* d_
     else { if (h) FGC_LAUNCH_FC(float, false, true); else FGC_LAUNCH_FC(float, false, false); }
   }
 #undef FGC_LAUNCH_FC
+#undef FGC_LAUNCH_FP
   FGC_LAUNCHED(1);
   return FGC_OK;
 }
@@ -1424,9 +1443,11 @@ fgc_status launch_fused_decode(const FusedTables* t, const ChunkInfo* d_chunks, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    FGC_CUDA(cudaLaunchKernelEx(&cfg, k_fused_decode, a));
+    if (pw.dtab) FGC_CUDA(cudaLaunchKernelEx(&cfg, k_fused_decode<true>, a));
+    else FGC_CUDA(cudaLaunchKernelEx(&cfg, k_fused_decode<false>, a));
   } else {
-    k_fused_decode<<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
+    if (pw.dtab) k_fused_decode<true><<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
+    else k_fused_decode<false><<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
   }
   FGC_LAUNCHED(1);
   return FGC_OK;
@@ -1444,7 +1465,7 @@ fgc_status launch_fused_inverse(const FusedTables* t, const ChunkInfo* d_chunks,
   a.t1024 = t->t1024;
   a.spectrum = spectrum;
   a.W = 0;
-  k_fused_decode<<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
+  k_fused_decode<false><<<2 * count, kThreads, sizeof(DecodeShared), s>>>(a);
   FGC_LAUNCHED(1);
   return FGC_OK;
 }
