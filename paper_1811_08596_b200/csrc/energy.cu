@@ -52,33 +52,39 @@ __device__ __forceinline__ double key_of(const T2* spec, uint64_t i) {
   return cabs_key((double)x.x, (double)x.y);
 }
 
-// numpy's pairwise_sum leaf (loops_utils.h.src): n <= 128 values a[0, n)
-__device__ double leaf_sum(const double* a, uint32_t n, double (*val)(const double*, uint32_t, const void*),
-                           const void* ctx) {
+// numpy's pairwise_sum leaf (loops_utils.h.src): n <= 128 values val(0..n-1)
+// (a functor, inlined: the 8 loads of an unrolled step are independent)
+template <class V>
+__device__ __forceinline__ double leaf_sum(uint32_t n, V val) {
   if (n < 8) {
     double res = 0.0;
-    for (uint32_t i = 0; i < n; ++i) res = __dadd_rn(res, val(a, i, ctx));
+    for (uint32_t i = 0; i < n; ++i) res = __dadd_rn(res, val(i));
     return res;
   }
   double r[8];
-  for (int j = 0; j < 8; ++j) r[j] = val(a, j, ctx);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = val(j);
   uint32_t i = 8;
-  for (; i < n - (n % 8u); i += 8)
-    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], val(a, i + j, ctx));
+  for (; i < n - (n % 8u); i += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = val(i + j);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v[j]);
+  }
   double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; ++i) res = __dadd_rn(res, val(a, i, ctx));
+  for (; i < n; ++i) res = __dadd_rn(res, val(i));
   return res;
 }
 
-struct LeafCtx {
-  uint32_t off, L, B;
-};
-// energy of bin off + i from the stored keys
-__device__ double energy_val(const double* keys, uint32_t i, const void* c) {
-  const LeafCtx& x = *static_cast<const LeafCtx*>(c);
-  const double k = keys[i];
-  return bin_weight(x.off + i, x.L, x.B) * __dmul_rn(k, k);
+// energy of bin off + i from the stored keys (spectral.py:150)
+__device__ __forceinline__ double leaf_energy_sum(const double* __restrict__ keys, uint32_t off, uint32_t n,
+                                                  uint32_t L, uint32_t B) {
+  return leaf_sum(n, [&](uint32_t i) {
+    const double k = keys[off + i];
+    return bin_weight(off + i, L, B) * __dmul_rn(k, k);
+  });
 }
 
 // The pairwise tree as an explicit post-order walk by one thread (mode 2:
@@ -94,11 +100,7 @@ __device__ double pairwise_walk(int mode, uint32_t n, uint32_t* loff, uint32_t* 
   while (fp) {
     F& f = fs[fp - 1];
     if (f.n <= 128) {
-      double res = 0.0;
-      {
-        LeafCtx c{f.off, L, B};
-        res = leaf_sum(keys + f.off, f.n, energy_val, &c);
-      }
+      const double res = leaf_energy_sum(keys, f.off, f.n, L, B);
       ++leaf;
       vals[vp++] = res;
       --fp;
@@ -134,7 +136,7 @@ struct __align__(16) ESh {
   double scan_d[kET / 32 + 1];
   unsigned long long scan_u[kET / 32 + 1];
   uint32_t scan[40];
-  uint32_t wcount, fbin, kcut, fallback;
+  uint32_t wcount, fbin, kcut, fallback, nleaf;
   double total, fbelow_e;
   unsigned long long fbelow_u;
 };
@@ -196,8 +198,16 @@ __global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, 
   const T2* sp = spectrum + ci.bin_off;
   double* K = keys + ci.bin_off;
   uint8_t* D = drop + ci.bin_off;
-  if (t == 0) { sh.wcount = 0; sh.fallback = 0; }
-  for (uint32_t b = t; b < B; b += kET) K[b] = key_of(sp, b);
+  if (t == 0) { sh.wcount = 0; sh.fallback = 0; sh.nleaf = 0; }
+  for (uint32_t b0 = t; b0 < B; b0 += 4 * kET) {      // the loads of 4 bins in flight together
+    T2 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (b0 + u * kET < B) x[u] = sp[b0 + u * kET];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (b0 + u * kET < B) K[b0 + u * kET] = cabs_key((double)x[u].x, (double)x[u].y);
+  }
   for (uint32_t b = t; b < kEB; b += kET) { sh.cnt[b] = 0; sh.sum[b] = 0; }
   __syncthreads();
   if (theta == 0.0) {                            // spectral.py:135-136: nothing dropped
@@ -230,12 +240,43 @@ __global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, 
     deeper = __syncthreads_or(split);
   }
   if (!deeper) {
+    // The leaves (0 < n <= 128; at most 2^kTreeDepth = kWin of them) are
+    // listed in the window index array (free until the window pass), then
+    // summed by 8 lanes each: lane j runs numpy's accumulator r[j] over
+    // elements j, j+8, ... (its loads issued together), the unrolled loop's
+    // final ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) is a 3-step xor shuffle
+    // (commutative adds: the same bits), and lane 0 adds the n % 8 tail.
     const uint32_t nodes = (2u << depth) - 1;
     for (uint32_t nd = t; nd < nodes; nd += kET) {
       const uint32_t n = sh.hn[nd];
-      if (n && n <= 128) {
-        LeafCtx cx{sh.hoff[nd], L, B};
-        sh.hval[nd] = leaf_sum(K + sh.hoff[nd], n, energy_val, &cx);
+      if (n && n <= 128) sh.widx[atomicAdd(&sh.nleaf, 1u)] = nd;
+    }
+    __syncthreads();
+    const uint32_t nl = sh.nleaf;
+    for (uint32_t base = 0; base < 8u * nl; base += kET) {      // uniform trip count: whole-warp shuffles
+      const uint32_t task = base + t, j = t & 7u;
+      const bool act = task < 8u * nl;
+      const uint32_t nd = act ? sh.widx[task >> 3] : 0u;
+      const uint32_t n = act ? sh.hn[nd] : 0u, off = act ? sh.hoff[nd] : 0u;
+      const uint32_t m8 = n >= 8u ? n - (n % 8u) : 0u;
+      auto val = [&](uint32_t i) {
+        const double k = K[off + i];
+        return bin_weight(off + i, L, B) * __dmul_rn(k, k);
+      };
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = (8u * q + j < m8) ? val(8u * q + j) : 0.0;
+      double r = v[0];
+#pragma unroll
+      for (int q = 1; q < 16; ++q)
+        if (8u * q < m8) r = __dadd_rn(r, v[q]);
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+      if (act && j == 0) {
+        double res = m8 ? r : 0.0;
+        for (uint32_t i = m8; i < n; ++i) res = __dadd_rn(res, val(i));
+        sh.hval[nd] = res;
       }
     }
     __syncthreads();
@@ -258,31 +299,41 @@ __global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, 
   //      native 32-bit shared-memory atomics, order-free; truncation costs at
   //      most B 2^-31 of the total, below one sub-bucket's energy, and the
   //      window keeps two sub-buckets of margin each side)
-  auto hi32 = [&](uint32_t b) { return (uint32_t)((unsigned long long)__double_as_longlong(K[b]) >> 32); };
+  const uint32_t* Kh = reinterpret_cast<const uint32_t*>(K) + 1;   // high word of key b at Kh[2b]
+  auto hi32 = [&](uint32_t b) { return Kh[2 * b]; };
+  // f(b, hi32(b)) over the chunk's bins, 4 high-word loads in flight per thread
+  auto for_hi = [&](auto f) {
+    for (uint32_t b0 = t; b0 < B; b0 += 4 * kET) {
+      uint32_t h[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) h[u] = (b0 + u * kET < B) ? hi32(b0 + u * kET) : 0u;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (b0 + u * kET < B) f(b0 + u * kET, h[u]);
+    }
+  };
   const double fscale = sh.total > 0.0 ? 0x1p31 / sh.total : 0.0;
   auto approx_e = [&](uint32_t h, uint32_t b) -> uint32_t {
     const double k = __hiloint2double((int)h, 0);
     return (uint32_t)fmin(bin_weight(b, L, B) * k * k * fscale, 0x1p31);
   };
   const unsigned long long ubudget = (unsigned long long)fmin(budget * fscale, 0x1p62);
-  for (uint32_t b = t; b < B; b += kET) {
-    const uint32_t h = hi32(b);
+  for_hi([&](uint32_t b, uint32_t h) {
     atomicAdd(&sh.cnt[h >> 20], 1u);
     atomicAdd(&sh.sum[h >> 20], approx_e(h, b));
-  }
+  });
   __syncthreads();
   uint32_t b1;
   unsigned long long e1;
   energy_bucket(sh, ubudget, b1, e1);
   for (uint32_t b = t; b < kEB; b += kET) { sh.cnt[b] = 0; sh.sum[b] = 0; }
   __syncthreads();
-  for (uint32_t b = t; b < B; b += kET) {
-    const uint32_t h = hi32(b);
+  for_hi([&](uint32_t b, uint32_t h) {
     if ((h >> 20) == b1) {
       atomicAdd(&sh.cnt[(h >> 9) & 2047u], 1u);
       atomicAdd(&sh.sum[(h >> 9) & 2047u], approx_e(h, b));
     }
-  }
+  });
   __syncthreads();
   uint32_t b2;
   unsigned long long e2;
@@ -293,22 +344,29 @@ __global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, 
   const uint32_t base = (b1 << 20) | (b2 << 9);
   const uint32_t wlo = base >= 1024u ? base - 1024u : 0u;
   const uint32_t whi = base + 1536u;
-  double below = 0.0;
+  // Everything below the window is dropped: its mask is written here, and
+  // its energy is taken as the total minus the energies at or above the
+  // window (a few percent of the bins, the only full keys loaded).  That
+  // prefix is as accurate as a direct sum to within the rounding tolerance
+  // the cut applies (below), which covers B u S.
+  double below = 0.0;                            // (holds the energy at or above the window until reduced)
   uint32_t nbelow = 0;
-  for (uint32_t b = t; b < B; b += kET) {
-    const uint32_t h = hi32(b);
+  for_hi([&](uint32_t b, uint32_t h) {
+    D[b] = h < wlo ? 1u : 0u;
     if (h < wlo) {
+      ++nbelow;
+    } else {
       const double k = K[b];
       below += bin_weight(b, L, B) * __dmul_rn(k, k);
-      ++nbelow;
-    } else if (h < whi) {
-      const uint32_t s = atomicAdd(&sh.wcount, 1u);
-      if (s < kWin) {
-        sh.wkey[s] = (unsigned long long)__double_as_longlong(K[b]);
-        sh.widx[s] = b;
+      if (h < whi) {
+        const uint32_t s = atomicAdd(&sh.wcount, 1u);
+        if (s < kWin) {
+          sh.wkey[s] = (unsigned long long)__double_as_longlong(k);
+          sh.widx[s] = b;
+        }
       }
     }
-  }
+  });
   // block sums of `below` (fp64) and `nbelow`
   {
     const uint32_t lane = t & 31, warp = t >> 5;
@@ -322,7 +380,7 @@ __global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, 
       double s = 0.0;
       uint32_t n = 0;
       for (int w = 0; w < kET / 32; ++w) { s += sh.scan_d[w]; n += sh.scan[w]; }
-      sh.fbelow_e = s;
+      sh.fbelow_e = fmax(sh.total - s, 0.0);
       sh.kcut = n;
     }
     __syncthreads();
@@ -377,10 +435,9 @@ __global__ void __launch_bounds__(kET) k_energy_select(const ChunkInfo* chunks, 
     }
     return;
   }
-  // ---- the drop mask: below the window, and the first kcut window entries
+  // ---- the drop mask (below the window: written above): the first kcut
+  //      window entries
   const uint32_t kw = sh.kcut;
-  for (uint32_t b = t; b < B; b += kET) D[b] = hi32(b) < wlo ? 1u : 0u;
-  __syncthreads();
   for (uint32_t i = t; i < m; i += kET) D[sh.hoff[i]] = i < kw ? 1u : 0u;
   if (t == 0) fb[c] = 0;
 }
