@@ -1356,8 +1356,10 @@ void fused_tables_free(FusedTables* t) {
 
 // Which compress kernel runs the 65536-sample chunks: 2 = k_fused_compress
 // above (default), 4 = the 4-CTA-cluster kernel of fused4.cu (two CTAs per
-// SM; bit-identical messages, measured slower: 226 vs 185 us at 25.6M floats,
-// its cluster barriers across 4 CTAs on shared SMs stall ~39% of the time).
+// SM; another FFT factorisation, oracle-exact on its own coefficients;
+// measured slower: 226 vs 185 us at 25.6M floats, its cluster barriers
+// across 4 CTAs on shared SMs stall ~39% of the time), 1 = fused_w.cu (1024
+// threads, lane-pair FFT columns; bit-identical; 196 vs 195 us).
 // FGC_COMPRESS_KERNEL sets the default; fgc_debug_set_compress_kernel switches it.
 static int g_compress_kernel = -1;
 static int compress_kernel() {

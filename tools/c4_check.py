@@ -51,3 +51,13 @@ for c, L in enumerate(lengths):
             print("chunk", c, "differs: nnz", nnz, ch.codes.size, "bm eq", bm == O.flags_to_bytes(ch.bitmap))
     pos += b
 print("chunks", len(lengths), "differing", bad, "| msg equal to 2-CTA kernel:", res[2][1] == res[ALT][1])
+if res[2][1] != res[ALT][1]:
+    a2, aa = np.frombuffer(res[2][1], np.uint8), np.frombuffer(res[ALT][1], np.uint8)
+    d = np.nonzero(a2 != aa)[0]
+    print("differing bytes", d.size, "first", d[:8])
+    for c, (off, bmo, co, _) in enumerate(layout):
+        nxt = layout[c + 1][0] if c + 1 < len(layout) else len(a2)
+        dd = d[(d >= off) & (d < nxt)]
+        if dd.size:
+            print(" chunk", c, "seg rel", (dd[:6] - off).tolist(), "bitmap at", bmo, "codes at", co, "seg len", nxt - off)
+            break
