@@ -1478,3 +1478,29 @@ extern "C" int fgc_debug_set_compress_kernel(int k) {
   fgc::g_compress_kernel = (k == 4 || k == 1) ? k : 2;
   return 0;
 }
+
+// Diagnostics: 2-CTA clusters of the fused compress / decode that fit the GPU
+// at once (cudaOccupancyMaxActiveClusters; the wave size of the fused grids).
+extern "C" int fgc_debug_fused_max_clusters(int which) {
+  using namespace fgc;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * 1024);
+  cfg.blockDim = dim3(kThreads);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = -1;
+  cudaError_t e;
+  if (which == 0) {
+    cfg.dynamicSmemBytes = sizeof(CompressShared);
+    e = cudaOccupancyMaxActiveClusters(&n, k_fused_compress<float, false, false>, &cfg);
+  } else {
+    cfg.dynamicSmemBytes = sizeof(DecodeShared);
+    e = cudaOccupancyMaxActiveClusters(&n, k_fused_decode<false>, &cfg);
+  }
+  return e == cudaSuccess ? n : -(int)e;
+}
