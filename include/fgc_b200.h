@@ -349,7 +349,12 @@ fgc_status fgc_exchange_average(fgc_plan* plan, fgc_exchange* x, const void* gra
  * average run on copy streams in pieces of consecutive chunks, overlapped
  * with the codec kernels.  x = NULL: single rank (message is this rank's
  * device message buffer); otherwise the peer exchange (message ignored).
- * dev_grad (n values of dtype) and dev_out (n floats) are device scratch. */
+ * dev_grad (n values of dtype) and dev_out (n floats) are device scratch.
+ * dev_grad belongs to this plan's host steps: a call's host->device copy of
+ * a piece waits only until the previous call's compress has read that
+ * piece (not for other work on `stream`), so back-to-back calls overlap one
+ * step's copy-out with the next step's copy-in (FGC_HOST_SERIAL=1: wait for
+ * everything earlier on `stream`).  host_out is complete once `stream` is. */
 fgc_status fgc_average_host(fgc_plan* plan, fgc_exchange* x, const void* host_grad, int dtype,
                             const double* weights, void* dev_grad, uint8_t* message, float* dev_out,
                             float* host_out, uint32_t* flags, void* stream);

@@ -91,6 +91,9 @@ struct fgc_plan {
   // host-buffer averaging: copy streams and per-piece events (created on first use)
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> ev_h, ev_c2, ev_d;
+  // host step: piece i of dev_grad fully read by the last call's compress
+  // (the next call's host->device copy of piece i waits only for that)
+  std::vector<cudaEvent_t> ev_cin;
   cudaEvent_t ev_step = nullptr;
   // pipelined allgather-average: exchange stream + per-piece events (created on first use)
   cudaStream_t xstream = nullptr;
@@ -302,6 +305,7 @@ extern "C" void fgc_plan_destroy(fgc_plan* p) {
   for (cudaEvent_t e : p->ev_h) cudaEventDestroy(e);
   for (cudaEvent_t e : p->ev_c2) cudaEventDestroy(e);
   for (cudaEvent_t e : p->ev_d) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_cin) cudaEventDestroy(e);
   if (p->ev_step) cudaEventDestroy(p->ev_step);
   if (p->h2d) cudaStreamDestroy(p->h2d);
   if (p->d2h) cudaStreamDestroy(p->d2h);
@@ -1031,6 +1035,12 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
     p->ev_c2.push_back(b);
     p->ev_d.push_back(c);
   }
+  const bool overlap_steps = !getenv("FGC_HOST_SERIAL");
+  while (p->ev_cin.size() < Pmax + 1) {
+    cudaEvent_t a;
+    FGC_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    p->ev_cin.push_back(a);
+  }
   int k = 0;
   uint32_t tval = 0;
   uint8_t* gathered = message;
@@ -1048,9 +1058,14 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
   auto d2h = [&](uint64_t lo, uint64_t hi) {
     return cudaMemcpyAsync(host_out + lo, dev_out + lo, (hi - lo) * sizeof(float), cudaMemcpyDeviceToHost, p->d2h);
   };
-  // the copy streams reuse dev_grad / dev_out only after the work already on s
+  // The copy-out stream follows the work already on s.  The copy-in of a
+  // piece waits only until the previous call's compress has read that piece
+  // of dev_grad (scratch of this call sequence), so consecutive steps
+  // overlap: step e+1's host->device copies run while step e's results are
+  // still copied out (the two directions of PCIe at once).  FGC_HOST_SERIAL=1
+  // makes the copy-in wait for all earlier work on s instead.
   FGC_CUDA(cudaEventRecord(p->ev_step, s));
-  FGC_CUDA(cudaStreamWaitEvent(p->h2d, p->ev_step, 0));
+  if (!overlap_steps) FGC_CUDA(cudaStreamWaitEvent(p->h2d, p->ev_step, 0));
   FGC_CUDA(cudaStreamWaitEvent(p->d2h, p->ev_step, 0));
 
   // generic chunks (all of them for energy mode / plans without fused
@@ -1065,11 +1080,13 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
   const uint64_t m_lo = pieces ? p->seg_off[p->fused_first + p->fused_count] : 0;
   cudaStream_t g = P ? p->side : s;
   if (generic) {
+    if (overlap_steps) FGC_CUDA(cudaStreamWaitEvent(p->h2d, p->ev_cin[Pmax], 0));
     FGC_CUDA(h2d(g_lo, p->desc.n));
     FGC_CUDA(cudaEventRecord(p->ev_h[P], p->h2d));
     FGC_CUDA(cudaStreamWaitEvent(g, p->ev_h[P], 0));
     if (energy) FGC_TRY(energy_compress(p, dev_grad, dtype, nullptr, message, nullptr, flags, g));
     else FGC_TRY(compress_range(p, dev_grad, dtype, message, flags, g, 0, 0, true));
+    FGC_CUDA(cudaEventRecord(p->ev_cin[Pmax], g));
     if (x) {
       FGC_CUDA(cudaEventRecord(p->ev_c2[P], g));
       if (energy)
@@ -1103,6 +1120,7 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
   auto seg_hi = [&](uint32_t i) -> uint64_t { return i + 1 == P ? m_lo : p->seg_off[f[i + 1]]; };
   exchange_trace(p->h2d, "start");
   for (uint32_t i = 0; i < P; ++i) {
+    if (overlap_steps) FGC_CUDA(cudaStreamWaitEvent(p->h2d, p->ev_cin[i], 0));
     FGC_CUDA(h2d(elem_lo(i), elem_hi(i)));
     FGC_CUDA(cudaEventRecord(p->ev_h[i], p->h2d));
     exchange_trace(p->h2d, "h2d");
@@ -1110,6 +1128,7 @@ static fgc_status average_host_impl(fgc_plan* p, fgc_exchange* x, const void* ho
   for (uint32_t i = 0; i < P; ++i) {
     FGC_CUDA(cudaStreamWaitEvent(s, p->ev_h[i], 0));
     FGC_TRY(compress_range(p, dev_grad, dtype, message, flags, s, f[i], f[i + 1] - f[i], false));
+    FGC_CUDA(cudaEventRecord(p->ev_cin[i], s));
     if (x) {
       FGC_CUDA(cudaEventRecord(p->ev_c2[i], s));
       FGC_TRY(exchange_publish_event(x, k, p->seg_off[f[i]], seg_hi(i) - p->seg_off[f[i]], p->ev_c2[i], tval,

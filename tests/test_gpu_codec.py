@@ -817,6 +817,31 @@ def test_step_host_matches_device_step(n, mode, dt):
     assert rel_l2(ref.double().numpy(), want) <= 1e-5
 
 
+@pytest.mark.parametrize("n,mode", [(12 * 65536 + 40960, "count"), (5 * 65536 + 99, "energy"), (40000, "count")])
+def test_step_host_back_to_back(n, mode):
+    """Consecutive host steps queued without waiting (wait=False) overlap:
+    step e+1's host->device copy of a piece starts once step e's compress has
+    read that piece, while step e's results are still copied out.  Every
+    step must still see its own input and produce its own output."""
+    from paper_1811_08596_b200.comm import GradientAverager
+    rng = np.random.default_rng(n + 5)
+    K = 5
+    gs = [(rng.standard_normal(n) * 1e-2 * (1 + k)).astype(np.float32) for k in range(K)]
+    q = F.calibrate([gs[-1]], 8, 3)
+    avg = GradientAverager(n, F.CodecConfig(F.SparsificationSpec(0.9, mode), q), [1.0])
+    refs = [avg.step(torch.from_numpy(g).cuda()).cpu() for g in gs]
+    hins = [torch.from_numpy(g).pin_memory() for g in gs]
+    houts = [torch.full((n,), float("nan"), dtype=torch.float32).pin_memory() for _ in gs]
+    for rep in range(2):
+        for k in range(K):
+            avg.step_host(hins[k], houts[k], wait=False)
+        torch.cuda.synchronize()
+        for k in range(K):
+            assert torch.equal(houts[k], refs[k]), (rep, k)
+            houts[k].fill_(float("nan"))
+    avg.check()
+
+
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
 def test_unaligned_views_are_realigned(dt):
     """A tensor view starting off the kernels' two-sample alignment is copied

@@ -30,3 +30,17 @@ lines = buf.value.decode().strip().splitlines()
 print(" | ".join(f"{l.split()[0]} {float(l.split()[1]):.3f}" for l in lines))
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 os.environ.pop("FGC_EXCHANGE_TRACE")
+# back-to-back steps queued without waiting (argv[2] = K): the cross-step
+# overlap of one step's copy-out with the next step's copy-in
+if len(sys.argv) > 2:
+    K = int(sys.argv[2])
+    os.environ["FGC_EXCHANGE_TRACE"] = "1"
+    torch.cuda.synchronize()
+    lib.fgc_debug_exchange_trace(buf, len(buf))          # clear
+    for it in range(K):
+        avg.step_host(hin, hout, wait=False)
+    torch.cuda.synchronize()
+    lib.fgc_debug_exchange_trace(buf, len(buf))
+    lines = buf.value.decode().strip().splitlines()
+    print(f"{K} back-to-back steps:")
+    print(" | ".join(f"{l.split()[0]} {float(l.split()[1]):.3f}" for l in lines))
