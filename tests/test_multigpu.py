@@ -112,6 +112,28 @@ def test_compressed_average_two_ranks(n, transport, mode):
     assert len({d for _, _, d in res}) == 1, "ranks disagree bitwise"
 
 
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
+@pytest.mark.parametrize("transport,mode", [("peer", "count"), ("peer-direct", "count"), ("peer-kpush", "count"),
+                                            ("nccl", "count"), ("peer", "energy")])
+def test_compressed_average_four_ranks(transport, mode):
+    """The same steps on 4 ranks: every rank decodes 4 messages in worker
+    order; results within 1e-5 of the oracle average and bitwise equal."""
+    import torch.multiprocessing as mp
+    world, n = 4, 5 * 65536 + 40960
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, transport, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=400)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    res = [q.get(timeout=10) for _ in range(world)]
+    assert all(rel <= 1e-5 for _, rel, _ in res), res
+    assert len({d for _, _, d in res}) == 1, "ranks disagree bitwise"
+
+
 @pytest.mark.parametrize("transport", ["peer", "peer-direct", "peer-kpush"])
 @pytest.mark.parametrize("seed", range(4))
 def test_random_configs_two_ranks(seed, transport):
