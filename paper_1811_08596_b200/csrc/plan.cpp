@@ -815,20 +815,6 @@ extern "C" fgc_status fgc_allgather_average(fgc_plan* p, void* comm, int nranks,
   return FGC_OK;
 }
 
-// Wave-aligned pieces of the fused chunk range: [f[i], f[i+1]), the remainder
-// (< 2 pieces) in the last one; the generic (tail) chunks ride with the last.
-static std::vector<uint32_t> wave_pieces(const fgc_plan* p, uint32_t waves) {
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint32_t per = std::max(1u, waves * (uint32_t)(sms / 2));
-  const uint32_t P = waves ? std::max(1u, p->fused_count / per) : 1u;
-  std::vector<uint32_t> f(P + 1);
-  for (uint32_t i = 0; i < P; ++i) f[i] = p->fused_first + i * per;
-  f[P] = p->fused_first + p->fused_count;
-  return f;
-}
-
 static fgc_status exchange_not_ready(const fgc_exchange* x) {
   set_error(exchange_poisoned(x) ? "exchange poisoned: an earlier step failed after it began publishing"
                                  : "exchange not opened");

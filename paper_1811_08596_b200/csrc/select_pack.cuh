@@ -143,7 +143,7 @@ __device__ __noinline__ void select_pack_chunk(SelectSharedT<TH>& sh, const Chun
                                                uint32_t* flags, const uint8_t* drop_mask) {
   const uint32_t B = ci.bins;
   const uint32_t kdrop = ci.drop;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
 
   int mode = kList;
   if (drop_mask) mode = kMask;                  // energy mode: the drop set is given
