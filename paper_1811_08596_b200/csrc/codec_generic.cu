@@ -25,19 +25,19 @@ inline uint32_t cdiv(uint64_t a, uint32_t b) { return (uint32_t)((a + b - 1) / b
 
 using namespace sel;
 
-template <typename CT>
-__global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* chunks, uint32_t first, Coeffs<CT> coeffs,
-                                                             int exact_only, QuantParams q, uint8_t* message,
-                                                             uint8_t* kept_mask, uint32_t* flags,
-                                                             const uint32_t* only_if, PieceCounter pc,
-                                                             const uint8_t* drop_mask) {
+template <typename CT, int TH = kSelThreads>
+__global__ void __launch_bounds__(TH) k_select_pack(const ChunkInfo* chunks, uint32_t first, Coeffs<CT> coeffs,
+                                                    int exact_only, QuantParams q, uint8_t* message,
+                                                    uint8_t* kept_mask, uint32_t* flags,
+                                                    const uint32_t* only_if, PieceCounter pc,
+                                                    const uint8_t* drop_mask) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SelectShared& sh = *reinterpret_cast<SelectShared*>(smem_raw);
+  SelectSharedT<TH>& sh = *reinterpret_cast<SelectSharedT<TH>*>(smem_raw);
   if (only_if && only_if[first + blockIdx.x] == 0u) return;
   const ChunkInfo ci = chunks[first + blockIdx.x];
   Coeffs<CT> cf = coeffs;
   cf.p += ci.bin_off;
-  select_pack_chunk(sh, ci, cf, exact_only, q, message, kept_mask, flags, drop_mask);
+  select_pack_chunk<CT, TH>(sh, ci, cf, exact_only, q, message, kept_mask, flags, drop_mask);
   if (pc.cnt) {                                  // segment complete: count it for the exchange
     __threadfence();
     __syncthreads();
@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select_pack(const ChunkInfo* ch
 
 constexpr int kDecThreads = 512;
 
+template <int kDecThreads>
 __global__ void __launch_bounds__(kDecThreads) k_decode_accumulate(const ChunkInfo* chunks, uint32_t first,
                                                                    const uint8_t* messages, int W, int w0, int G,
                                                                    uint64_t stride, Weights wts, QuantParams q,
@@ -110,10 +111,25 @@ fgc_status launch_select_pack(const ChunkInfo* d_chunks, uint32_t first, uint32_
   if (!count) return FGC_OK;
   static bool attr = false;
   const size_t smem = sizeof(SelectShared);
+  constexpr int kWide = 1024;
+  const size_t smem_w = sizeof(SelectSharedT<kWide>);
   if (!attr) {
     FGC_CUDA(cudaFuncSetAttribute(k_select_pack<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FGC_CUDA(cudaFuncSetAttribute(k_select_pack<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FGC_CUDA(cudaFuncSetAttribute(k_select_pack<float2, kWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_w));
     attr = true;
+  }
+  // a few chunks (a plan's tail class beside the fused grid): one wide CTA
+  // each -- the chunk's select + pack is a latency chain of tiles, and the
+  // tail's kernel chain runs beside the fused grid on the side stream
+  static const int wide = [] { const char* e = getenv("FGC_WIDE_TAIL"); return e ? atoi(e) : 1; }();
+  if (!coeff_f64 && wide && count <= 4) {
+    Coeffs<float2> c{static_cast<const float2*>(spectrum)};
+    k_select_pack<float2, kWide><<<count, kWide, smem_w, s>>>(d_chunks, first, c, 0, q, message, kept_mask, flags,
+                                                              only_if, pc, drop_mask);
+    FGC_LAUNCHED(1);
+    return FGC_OK;
   }
   if (coeff_f64) {
     Coeffs<double2> c{static_cast<const double2*>(spectrum)};
@@ -224,12 +240,21 @@ fgc_status launch_decode_accumulate(const ChunkInfo* d_chunks, uint32_t first, u
   }
   static bool attr = false;
   if (!attr) {
-    FGC_CUDA(cudaFuncSetAttribute(k_decode_accumulate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
+    FGC_CUDA(cudaFuncSetAttribute(k_decode_accumulate<kDecThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)budget));
+    FGC_CUDA(cudaFuncSetAttribute(k_decode_accumulate<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)budget));
     attr = true;
   }
   for (int w0 = 0; w0 < W; w0 += G) {
     const size_t smem = (size_t)G * bm_words * 4;
-    k_decode_accumulate<<<count, kDecThreads, smem, s>>>(d_chunks, first, messages, W, w0, G, stride, wts, q, spectrum);
+    static const int wide = [] { const char* e = getenv("FGC_WIDE_TAIL"); return e ? atoi(e) : 1; }();
+    if (wide && count <= 4)          // a few chunks (a plan's tail class): one wide CTA each
+      k_decode_accumulate<1024><<<count, 1024, smem, s>>>(d_chunks, first, messages, W, w0, G, stride, wts, q,
+                                                          spectrum);
+    else
+      k_decode_accumulate<kDecThreads><<<count, kDecThreads, smem, s>>>(d_chunks, first, messages, W, w0, G, stride,
+                                                                        wts, q, spectrum);
     FGC_LAUNCHED(1);
   }
   return FGC_OK;
