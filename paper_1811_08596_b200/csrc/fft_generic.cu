@@ -74,18 +74,28 @@ __global__ void k_init_bluestein_b(typename V2<R>::T* b, const typename V2<R>::T
   b[e] = v;
 }
 
-// Stockham radix-2 over `nt` transforms of size S held in shared memory.
+// W_S^j, j < S/2, from the global table of W_twP into shared memory (the
+// same values: every stage then reads its twiddles without an L2 round
+// trip, which dominated small transforms' stages).  Caller syncs.
 template <class T2>
-__device__ T2* smem_stockham(T2* x, T2* y, uint32_t S, uint32_t nt, const T2* tw, uint32_t twP, int dir) {
+__device__ __forceinline__ void load_stage_twiddles(T2* stw, uint32_t S, const T2* tw, uint32_t twP) {
+  const uint32_t step = twP / S;
+  for (uint32_t j = threadIdx.x; j < (S >> 1); j += blockDim.x) stw[j] = tw[(uint64_t)j * step];
+}
+
+// Stockham radix-2 over `nt` transforms of size S held in shared memory;
+// stw = W_S^j (j < S/2) in shared memory.
+template <class T2>
+__device__ T2* smem_stockham(T2* x, T2* y, uint32_t S, uint32_t nt, const T2* stw, int dir) {
   const uint32_t half = S >> 1;
   const uint32_t lhalf = __ffs(half) - 1;
   for (uint32_t p = 1; p < S; p <<= 1) {
-    const uint32_t twstride = twP / (2 * p);
+    const uint32_t twstride = S / (2 * p);
     for (uint32_t b = threadIdx.x; b < nt * half; b += blockDim.x) {
       const uint32_t t = b >> lhalf, i = b & (half - 1);
       const uint32_t k = i & (p - 1);
       const T2 u0 = x[t * S + i];
-      T2 w = tw[(uint64_t)k * twstride];
+      T2 w = stw[k * twstride];
       if (dir > 0) w.y = -w.y;
       const T2 u1 = zmul(x[t * S + i + half], w);
       const uint32_t o = t * S + ((i - k) << 1) + k;
@@ -111,10 +121,12 @@ __global__ void __launch_bounds__(NT) k_smem_fft(T2* data, uint32_t S, uint32_t 
   const uint32_t nt = (uint32_t)min((uint64_t)per_cta, total - first);
   T2* x = sm;
   T2* y = sm + (size_t)per_cta * S;
+  T2* stw = y + (size_t)per_cta * S;
   T2* g = data + first * S;
+  load_stage_twiddles(stw, S, tw, twP);
   for (uint32_t e = threadIdx.x; e < nt * S; e += blockDim.x) x[e] = g[e];
   __syncthreads();
-  T2* r = smem_stockham(x, y, S, nt, tw, twP, dir);
+  T2* r = smem_stockham(x, y, S, nt, stw, dir);
   for (uint32_t e = threadIdx.x; e < nt * S; e += blockDim.x) g[e] = r[e];
 }
 
@@ -134,6 +146,8 @@ __global__ void __launch_bounds__(kFftThreads) k_col_fft(T2* data, uint32_t Rr, 
   T2* g = data + item * P;
   T2* x = sm;
   T2* y = sm + (size_t)G * Rr;
+  T2* stw = y + (size_t)G * Rr;
+  load_stage_twiddles(stw, Rr, tw, twP);
   for (uint32_t e = threadIdx.x; e < G * Rr; e += blockDim.x) {
     const uint32_t r = e / G, cg = e % G;            // coalesced along columns
     T2 v = g[(uint64_t)r * C + c0 + cg];
@@ -145,7 +159,7 @@ __global__ void __launch_bounds__(kFftThreads) k_col_fft(T2* data, uint32_t Rr, 
     x[cg * Rr + r] = v;
   }
   __syncthreads();
-  T2* res = smem_stockham(x, y, Rr, G, tw, twP, dir);
+  T2* res = smem_stockham(x, y, Rr, G, stw, dir);
   for (uint32_t e = threadIdx.x; e < G * Rr; e += blockDim.x) {
     const uint32_t r = e / G, cg = e % G;
     T2 v = res[cg * Rr + r];
@@ -287,7 +301,7 @@ fgc_status pow2_rec(typename V2<R>::T* data, uint64_t batch, uint32_t P, const t
     // transforms per CTA: up to a full shared-memory tile, but small batches
     // are spread over the SMs (latency, not throughput, rules there)
     const uint32_t per = max(1u, min(cap / P, (uint32_t)((batch + 295) / 296)));
-    const size_t smem = 2ull * per * P * sizeof(T2);
+    const size_t smem = (2ull * per * P + P / 2) * sizeof(T2);
     const uint32_t ctas = ceil_div(batch, per);
     if (ctas < 148 && P * per >= 4096)
       k_smem_fft<T2, 1024><<<ctas, 1024, smem, s>>>(data, P, per, batch, tw, twP, dir);
@@ -299,7 +313,7 @@ fgc_status pow2_rec(typename V2<R>::T* data, uint64_t batch, uint32_t P, const t
   uint32_t Rr, C;
   fft_split(P, cap, Rr, C);
   const uint32_t G = max(1u, min(C, cap / Rr));
-  const size_t col_smem = 2ull * G * Rr * sizeof(T2);
+  const size_t col_smem = (2ull * G * Rr + Rr / 2) * sizeof(T2);
   const uint64_t cols = batch * (C / G);
   if (cols > 0x7FFFFFFFull) { set_error("transform batch too large"); return FGC_ERR_UNSUPPORTED; }
   if (dir < 0) {
@@ -325,7 +339,7 @@ fgc_status set_attrs() {
   using T2 = typename V2<R>::T;
   static bool done = false;
   if (done) return FGC_OK;
-  const int bytes = (int)(2 * smem_points(sizeof(R)) * sizeof(T2));
+  const int bytes = (int)((2 * smem_points(sizeof(R)) + smem_points(sizeof(R)) / 2) * sizeof(T2));
   FGC_CUDA(cudaFuncSetAttribute(k_smem_fft<T2, kFftThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   FGC_CUDA(cudaFuncSetAttribute(k_smem_fft<T2, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   FGC_CUDA(cudaFuncSetAttribute(k_col_fft<T2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
