@@ -126,3 +126,29 @@ def test_c3_alexnet_theta_sweep_full_message_bit_exact(theta):
 def test_c4_vgg16_bit_sweep_full_message_bit_exact(nm):
     """BASELINE config 4: 138M floats, 4/6/8/16-bit range floats."""
     _full_message_parity(138_000_000, 0.9, nm, seed=2)
+
+
+@pytest.mark.parametrize("kernel", [1, 4])
+def test_alternative_compress_kernels_full_message(kernel):
+    """The selectable compress variants (FGC_COMPRESS_KERNEL): 1 = 1024-thread
+    CTAs with lane-pair FFT columns (fused_w.cu), 4 = 4-CTA clusters
+    (fused4.cu).  Each is byte-exact against the oracle's encoding of its own
+    coefficients at C2 size; the 1024-thread kernel computes the same
+    coefficients as the default, so its message is byte-equal to the
+    default's too."""
+    import ctypes
+    from paper_1811_08596_b200 import _lib
+    setk = _lib.lib.fgc_debug_set_compress_kernel
+    setk.argtypes = [ctypes.c_int]
+    n = 25_600_000
+    g = torch.randn(n, device="cuda", generator=torch.Generator("cuda").manual_seed(0)) * 1e-2
+    q = F.calibrate([g[:CHUNK * 4].double().cpu().numpy()], 8, 3)
+    cfg = F.CodecConfig(F.SparsificationSpec(0.9), q, chunk_size=CHUNK)
+    default = debug.message_bytes(F.compress(g, cfg))
+    try:
+        setk(kernel)
+        if kernel == 1:
+            assert debug.message_bytes(F.compress(g, cfg)) == default
+        _full_message_parity(n, 0.9, (8, 3))
+    finally:
+        setk(2)
