@@ -426,7 +426,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="resnet50", choices=sorted(WORKLOADS))
-    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--n", "--n-floats", dest="n", type=int, default=None)
     ap.add_argument("--mode", default="count", choices=["count", "energy"],
                     help="sparsification rule (spectral.py:124-139); the headline is count mode")
     ap.add_argument("--theta-drop", type=float, default=None,
@@ -455,8 +455,11 @@ def main():
         with socket.socket() as sk:
             sk.bind(("127.0.0.1", 0))
             port = sk.getsockname()[1]
+        # (torch.distributed.run's own parser would take `--n` for an
+        # abbreviation of its options: pass it under its long alias)
+        fwd = ["--n-floats" + a[3:] if a == "--n" or a.startswith("--n=") else a for a in sys.argv[1:]]
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-               "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+               "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *fwd]
         sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
