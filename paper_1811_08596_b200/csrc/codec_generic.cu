@@ -14,6 +14,7 @@
 #include "fgc_device.cuh"
 #include "fgc_internal.h"
 #include "select_pack.cuh"
+#include "decode_acc.cuh"
 
 namespace fgc {
 
@@ -56,48 +57,8 @@ __global__ void __launch_bounds__(kDecThreads) k_decode_accumulate(const ChunkIn
                                                                    float2* spectrum) {
   extern __shared__ __align__(16) uint32_t pref[];    // G x bm_words exclusive popcount prefixes
   __shared__ uint32_t scan[40];
-  const ChunkInfo ci = chunks[first + blockIdx.x];
-  const uint32_t bm_words = (ci.slots + 31) / 32;
-  const uint32_t tid = threadIdx.x;
-  const int gn = min(G, W - w0);
-  // prefix tables: each thread owns a contiguous run of words
-  const uint32_t per = (bm_words + kDecThreads - 1) / kDecThreads;
-  for (int g = 0; g < gn; ++g) {
-    const uint32_t* bm = reinterpret_cast<const uint32_t*>(messages + (uint64_t)(w0 + g) * stride + ci.seg_off + kSegHeader);
-    uint32_t local = 0;
-    const uint32_t a = tid * per, b = min(bm_words, a + per);
-    for (uint32_t w = a; w < b; ++w) local += __popc(bm[w]);
-    uint32_t tot;
-    uint32_t base = block_exclusive_scan<kDecThreads>(local, scan, tot);
-    for (uint32_t w = a; w < b; ++w) {
-      pref[g * bm_words + w] = base;
-      base += __popc(bm[w]);
-    }
-  }
-  __syncthreads();
-  const int N = q.n_bits;
-  for (uint32_t i = tid; i < ci.bins; i += kDecThreads) {
-    float2 acc = make_float2(0.f, 0.f);
-    if (w0 > 0) acc = spectrum[ci.bin_off + i];
-    const uint32_t slot = 2 * i;
-    const uint32_t word = slot >> 5, sh = slot & 31u;
-    for (int g = 0; g < gn; ++g) {
-      const uint8_t* seg = messages + (uint64_t)(w0 + g) * stride + ci.seg_off;
-      const uint32_t* bm = reinterpret_cast<const uint32_t*>(seg + kSegHeader);
-      const uint32_t* cw = reinterpret_cast<const uint32_t*>(seg + ci.code_off);
-      const uint32_t sw = ballot_to_wire(bm[word]);          // slot order
-      const uint32_t bits = (sw >> sh) & 3u;
-      if (!bits) continue;
-      uint32_t r = pref[g * bm_words + word] + __popc(sw & ((1u << sh) - 1u));
-      float re = 0.f, im = 0.f;
-      if (bits & 1u) { re = decode_code(q, read_bits(cw, (uint64_t)r * N, N)); ++r; }
-      if (bits & 2u) im = decode_code(q, read_bits(cw, (uint64_t)r * N, N));
-      const float wt = wts.w[w0 + g];
-      acc.x = __fmaf_rn(wt, re, acc.x);
-      acc.y = __fmaf_rn(wt, im, acc.y);
-    }
-    spectrum[ci.bin_off + i] = acc;
-  }
+  decode_accumulate_chunk<kDecThreads>(chunks[first + blockIdx.x], messages, W, w0, G, stride, wts, q, spectrum,
+                                       pref, scan);
 }
 
 }  // namespace

@@ -133,6 +133,19 @@ template <class R>
 fgc_status real_inverse(RealClassT<R>& rc, const ChunkInfo* d_chunks, const typename Vec2<R>::T* spectrum, R* out,
                         cudaStream_t s);
 
+// The whole chain of one tail chunk in one 1024-thread CTA per direction
+// (real_fft.cu): forward transform + select + pack into `message`, and the
+// weighted decode of W messages + inverse transform into `out`.  Float
+// plans, one chunk, Pow2 (P <= 4096) or Mixed (B <= 4096) only.
+bool tail_chain_ok(const RealClassT<float>& rc);
+fgc_status tail_forward_chain(RealClassT<float>& rc, const ChunkInfo* d_chunks, const void* in, int in_dtype,
+                              int half_pass, uint32_t* flags, float2* spectrum, const QuantParams& q, uint8_t* message,
+                              cudaStream_t s);
+struct Weights;
+fgc_status tail_inverse_chain(RealClassT<float>& rc, const ChunkInfo* d_chunks, const uint8_t* messages, int W,
+                              uint64_t stride, const Weights& wts, const QuantParams& q, float2* spectrum, float* out,
+                              uint32_t max_slots, cudaStream_t s);
+
 // ---------------------------------------------------------------- codec kernels
 
 // Select (count mode) + quantize + pack from a chunk-major spectrum.

@@ -378,6 +378,19 @@ static fgc_status forward_generic(fgc_plan* p, const void* grad, int dtype, floa
   return FGC_OK;
 }
 
+// FGC_TAIL_CHAIN=1: the tail class beside the fused grid runs as one
+// single-CTA chain per direction (real_fft.cu) when every generic class
+// qualifies.  Bit-identical to the multi-kernel chain but measured slower
+// (0.363 vs 0.300 ms per step: its 183 / 131 us of latency per direction
+// end up on the critical path), so off by default.
+static bool tail_chain(const fgc_plan* p) {
+  static const bool on = [] { const char* e = getenv("FGC_TAIL_CHAIN"); return e && e[0] == '1'; }();
+  if (!on || !p->fused_count) return false;
+  for (const RealClass& rc : p->classes)
+    if (!rc.fused && !tail_chain_ok(rc)) return false;
+  return true;
+}
+
 static fgc_status check_mode(const fgc_plan* p) {
   if (p->desc.mode != FGC_MODE_COUNT && p->desc.mode != FGC_MODE_ENERGY) {
     set_error("unknown sparsification mode");
@@ -421,7 +434,11 @@ static fgc_status compress_range(fgc_plan* p, const void* grad, int dtype, uint8
     FGC_CUDA(cudaEventRecord(p->ev_fork, s));
     FGC_CUDA(cudaStreamWaitEvent(g, p->ev_fork, 0));
   }
-  if (generic) {
+  if (generic && tail_chain(p)) {
+    for (RealClass& rc : p->classes)
+      if (!rc.fused)
+        FGC_TRY(tail_forward_chain(rc, p->d_chunks, grad, dtype, p->desc.half_pass, flags, p->d_spec, p->q, message, g));
+  } else if (generic) {
     FGC_TRY(forward_generic(p, grad, dtype, p->d_spec, flags, g, false));
     for (RealClass& rc : p->classes) {
       if (rc.fused) continue;
@@ -502,7 +519,11 @@ static fgc_status decode_range(fgc_plan* p, const uint8_t* messages, int W, uint
     FGC_CUDA(cudaEventRecord(p->ev_fork, s));
     FGC_CUDA(cudaStreamWaitEvent(g, p->ev_fork, 0));
   }
-  if (generic) {
+  if (generic && tail_chain(p)) {
+    for (RealClass& rc : p->classes)
+      if (!rc.fused)
+        FGC_TRY(tail_inverse_chain(rc, p->d_chunks, messages, W, stride, w, p->q, p->d_spec, out, p->max_slots, g));
+  } else if (generic) {
     for (RealClass& rc : p->classes) {
       if (rc.fused) continue;
       FGC_TRY(launch_decode_accumulate(p->d_chunks, rc.first, rc.count, messages, W, stride, w, p->q, p->d_spec,

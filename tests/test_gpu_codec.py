@@ -980,3 +980,22 @@ def test_average_precision_fp32_weights_and_accumulation(W):
     rel = rel_l2(got, ref)
     print(f"W={W}: fused average vs float64 average of the same messages: rel-L2 {rel:.2e}")
     assert rel <= 1e-6
+
+
+def test_tail_chain_matches_kernel_chain():
+    """The single-CTA tail chain (FGC_TAIL_CHAIN=1, opt-in) runs the same
+    device code in the same order as the multi-kernel chain, so messages and
+    averages must be bit-identical to it (Pow2 and Mixed tails, f32 / f64
+    input, W = 1 / 3)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    probe = Path(__file__).resolve().parent / "_tail_chain_probe.py"
+    digests = []
+    for flag in ("0", "1"):
+        env = dict(os.environ, FGC_TAIL_CHAIN=flag)
+        r = subprocess.run([sys.executable, str(probe)], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        digests.append(r.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1], digests
