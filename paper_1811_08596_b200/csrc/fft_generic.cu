@@ -5,7 +5,7 @@
 // spectral.py:95,106, codec.py:463).
 //
 //   Direct     Lc <= 64            O(Lc^2) per signal, exact-reduced twiddles
-//   Pow2       Lc = 2^k            Stockham radix-2 in shared memory (<= 4096
+//   Pow2       Lc = 2^k            Stockham radix-4 in shared memory (<= 4096
 //                                  points), larger sizes by a four-step split
 //                                  through global memory (recursive on rows)
 //   Mixed      Lc = A 2^e, A odd    one direct pass over the odd factor (A <=
@@ -198,7 +198,7 @@ fgc_status pow2_rec(typename V2<R>::T* data, uint64_t batch, uint32_t P, const t
     // transforms per CTA: up to a full shared-memory tile, but small batches
     // are spread over the SMs (latency, not throughput, rules there)
     const uint32_t per = max(1u, min(cap / P, (uint32_t)((batch + 295) / 296)));
-    const size_t smem = (2ull * per * P + P / 2) * sizeof(T2);
+    const size_t smem = (2ull * per * P + stage_twiddles(P)) * sizeof(T2);
     const uint32_t ctas = ceil_div(batch, per);
     if (ctas < 148 && P * per >= 4096)
       k_smem_fft<T2, 1024><<<ctas, 1024, smem, s>>>(data, P, per, batch, tw, twP, dir);
@@ -210,7 +210,7 @@ fgc_status pow2_rec(typename V2<R>::T* data, uint64_t batch, uint32_t P, const t
   uint32_t Rr, C;
   fft_split(P, cap, Rr, C);
   const uint32_t G = max(1u, min(C, cap / Rr));
-  const size_t col_smem = (2ull * G * Rr + Rr / 2) * sizeof(T2);
+  const size_t col_smem = (2ull * G * Rr + stage_twiddles(Rr)) * sizeof(T2);
   const uint64_t cols = batch * (C / G);
   if (cols > 0x7FFFFFFFull) { set_error("transform batch too large"); return FGC_ERR_UNSUPPORTED; }
   if (dir < 0) {
@@ -236,7 +236,7 @@ fgc_status set_attrs() {
   using T2 = typename V2<R>::T;
   static bool done = false;
   if (done) return FGC_OK;
-  const int bytes = (int)((2 * smem_points(sizeof(R)) + smem_points(sizeof(R)) / 2) * sizeof(T2));
+  const int bytes = (int)((2 * smem_points(sizeof(R)) + stage_twiddles(smem_points(sizeof(R)))) * sizeof(T2));
   FGC_CUDA(cudaFuncSetAttribute(k_smem_fft<T2, kFftThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   FGC_CUDA(cudaFuncSetAttribute(k_smem_fft<T2, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   FGC_CUDA(cudaFuncSetAttribute(k_col_fft<T2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));

@@ -27,40 +27,62 @@ template <class T2> __device__ __forceinline__ T2 zadd(T2 a, T2 b) { return mk(a
 template <class T2> __device__ __forceinline__ T2 zsub(T2 a, T2 b) { return mk(a.x - b.x, a.y - b.y); }
 
 
-// W_S^j, j < S/2, from the global table of W_twP into shared memory (the
-// same values: every stage then reads its twiddles without an L2 round
-// trip, which dominated small transforms' stages).  Caller syncs.
+// W_S^j, j < 3S/4, from the global table of W_twP into shared memory (the
+// same values; every stage reads its twiddles without an L2 round trip).
+// Caller syncs.
+constexpr uint32_t stage_twiddles(uint32_t S) { return S - (S >> 2); }
 template <class T2>
 __device__ __forceinline__ void load_stage_twiddles(T2* stw, uint32_t S, const T2* tw, uint32_t twP) {
   const uint32_t step = twP / S;
-  for (uint32_t j = threadIdx.x; j < (S >> 1); j += blockDim.x) stw[j] = tw[(uint64_t)j * step];
+  for (uint32_t j = threadIdx.x; j < stage_twiddles(S); j += blockDim.x) stw[j] = tw[(uint64_t)j * step];
 }
 
-// Stockham radix-2 over `nt` transforms of size S held in shared memory;
-// stw = W_S^j (j < S/2) in shared memory.
+// Stockham autosort FFT over `nt` transforms of size S (a power of two)
+// held in shared memory: one radix-2 stage when log2 S is odd, then radix-4
+// stages (half the stages and barriers of radix-2; the quarter-turn of a
+// radix-4 butterfly is exact).  stw = W_S^j (j < 3S/4) in shared memory.
 template <class T2>
 __device__ T2* smem_stockham(T2* x, T2* y, uint32_t S, uint32_t nt, const T2* stw, int dir) {
-  const uint32_t half = S >> 1;
-  const uint32_t lhalf = __ffs(half) - 1;
-  for (uint32_t p = 1; p < S; p <<= 1) {
-    const uint32_t twstride = S / (2 * p);
+  const uint32_t lg = __ffs(S) - 1;
+  uint32_t p = 1;
+  if (lg & 1u) {                                      // radix-2 stage (p = 1: no twiddle)
+    const uint32_t half = S >> 1;
     for (uint32_t b = threadIdx.x; b < nt * half; b += blockDim.x) {
-      const uint32_t t = b >> lhalf, i = b & (half - 1);
-      const uint32_t k = i & (p - 1);
-      const T2 u0 = x[t * S + i];
-      T2 w = stw[k * twstride];
-      if (dir > 0) w.y = -w.y;
-      const T2 u1 = zmul(x[t * S + i + half], w);
-      const uint32_t o = t * S + ((i - k) << 1) + k;
+      const uint32_t t = b >> (lg - 1), i = b & (half - 1);
+      const T2 u0 = x[t * S + i], u1 = x[t * S + i + half];
+      const uint32_t o = t * S + (i << 1);
       y[o] = zadd(u0, u1);
-      y[o + p] = zsub(u0, u1);
+      y[o + 1] = zsub(u0, u1);
+    }
+    __syncthreads();
+    T2* tmp = x; x = y; y = tmp;
+    p = 2;
+  }
+  if (S < 4) return x;
+  const uint32_t q4 = S >> 2, lq = lg - 2;
+  for (; p < S; p <<= 2) {
+    const uint32_t ts = S / (4 * p);
+    for (uint32_t b = threadIdx.x; b < nt * q4; b += blockDim.x) {
+      const uint32_t t = b >> lq, i = b & (q4 - 1);
+      const uint32_t k = i & (p - 1);
+      const T2* xs = x + t * S + i;
+      const T2 x0 = xs[0];
+      T2 w1 = stw[k * ts], w2 = stw[2 * k * ts], w3 = stw[3 * k * ts];
+      if (dir > 0) { w1.y = -w1.y; w2.y = -w2.y; w3.y = -w3.y; }
+      const T2 a1 = zmul(xs[q4], w1), a2 = zmul(xs[2 * q4], w2), a3 = zmul(xs[3 * q4], w3);
+      const T2 t0 = zadd(x0, a2), t1 = zsub(x0, a2), t2 = zadd(a1, a3), d = zsub(a1, a3);
+      const T2 t3 = dir < 0 ? mk(d.y, -d.x) : mk(-d.y, d.x);         // (a1 - a3) * (-+i)
+      T2* yo = y + t * S + 4 * (i - k) + k;
+      yo[0] = zadd(t0, t2);
+      yo[p] = zadd(t1, t3);
+      yo[2 * p] = zsub(t0, t2);
+      yo[3 * p] = zsub(t1, t3);
     }
     __syncthreads();
     T2* tmp = x; x = y; y = tmp;
   }
   return x;
 }
-
 
 // Mixed-radix outer pass, Lc = A * B.  Index n = B n1 + n2, k = k1 + A k2.
 //   forward (dir < 0): Y[k1 B + n2] = W^(k1 n2) sum_n1 x[B n1 + n2] W_A^(k1 n1)
