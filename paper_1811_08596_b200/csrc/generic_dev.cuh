@@ -1,7 +1,7 @@
 // Device building blocks of the generic DFT engine (fft_generic.cu), shared
 // with the single-CTA tail chains (real_fft.cu) so both run the same
-// arithmetic: complex helpers, the shared-memory Stockham radix-2 pass and
-// one tile of the mixed-radix outer pass.
+// arithmetic: complex helpers, the shared-memory Stockham pass and one tile
+// of the mixed-radix outer pass.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
