@@ -43,7 +43,7 @@ def _check_chunk(c):
     s = _S
     L = s["lengths"][c]
     b0, b1 = s["bin_off"][c], s["bin_off"][c + 1]
-    kept, ch = O.encode_spectrum(s["spec"][b0:b1], L, s["theta"], "count", s["lat"])
+    kept, ch = O.encode_spectrum(s["spec"][b0:b1], L, s["theta"], s["mode"], s["lat"])
     off, bmo, co, _ = s["layout"][c]
     buf = s["msg"]
     nnz = int.from_bytes(buf[off:off + 4], "little")
@@ -78,10 +78,12 @@ def _pool_map(fn, items):
         return pool.map(fn, items, chunksize=max(1, len(items) // (8 * cores)))
 
 
-def _full_message_parity(n, theta, nm, seed=0):
+def _full_message_parity(n, theta, nm, seed=0, mode="count", half=False, f64=False):
     g = torch.randn(n, device="cuda", generator=torch.Generator("cuda").manual_seed(seed)) * 1e-2
+    if f64:
+        g = g.double()
     q = F.calibrate([g[:CHUNK * 4].double().cpu().numpy()], *nm)
-    cfg = F.CodecConfig(F.SparsificationSpec(theta), q, chunk_size=CHUNK)
+    cfg = F.CodecConfig(F.SparsificationSpec(theta, mode), q, half_precision_pass=half, chunk_size=CHUNK)
     m1 = F.compress(g, cfg)
     m2 = F.compress(g, cfg)
     b1, b2 = debug.message_bytes(m1), debug.message_bytes(m2)
@@ -92,9 +94,9 @@ def _full_message_parity(n, theta, nm, seed=0):
     spec = debug.forward_spectrum(g, cfg)
     lengths = O.chunk_lengths(n, CHUNK)
     bins = [L // 2 + 1 for L in lengths]
-    layout, total = O.device_layout(n, CHUNK, theta, nm[0])
+    layout, total = O.device_layout(n, CHUNK, theta, nm[0], mode)
     assert len(b1) == total
-    _S.update(spec=spec, msg=b1, out=out1.double().cpu().numpy(), theta=theta, width=nm[0],
+    _S.update(spec=spec, msg=b1, out=out1.double().cpu().numpy(), theta=theta, width=nm[0], mode=mode,
               lat=O.lattice(q.min, q.max, q.n_bits, q.mantissa_bits, q.eps), lengths=lengths,
               bin_off=np.concatenate([[0], np.cumsum(bins)]), in_off=np.concatenate([[0], np.cumsum(lengths)]),
               layout=layout)
@@ -104,7 +106,7 @@ def _full_message_parity(n, theta, nm, seed=0):
         _S.clear()
     bad = [r for r in res if not r[1]]
     worst = max(r[4] for r in res)
-    print(f"n={n} theta={theta} nm={nm}: {len(res)} chunks, {len(bad)} differ "
+    print(f"n={n} theta={theta} nm={nm} mode={mode} half={half} f64={f64}: {len(res)} chunks, {len(bad)} differ "
           f"(kept flips {sum(r[2] for r in bad)}, code diffs {sum(r[3] for r in bad)}), "
           f"worst per-chunk decode rel-L2 {worst:.2e}")
     assert not bad, bad[:5]
@@ -114,6 +116,14 @@ def _full_message_parity(n, theta, nm, seed=0):
 def test_c2_resnet50_full_message_bit_exact():
     """BASELINE config 2: 25.6M floats, keep 0.1, (8,3); all 391 chunks."""
     _full_message_parity(25_600_000, 0.9, (8, 3))
+
+
+@pytest.mark.parametrize("mode,half,f64", [("energy", False, False), ("count", True, False), ("count", False, True)])
+def test_c2_variants_full_message_bit_exact(mode, half, f64):
+    """C2 through the other code paths of the fused kernels: energy mode
+    (the energy drop set on the fused forward transform), the binary16
+    half-precision pass (the HALF load), float64 input (the double load)."""
+    _full_message_parity(25_600_000, 0.9, (8, 3), seed=3, mode=mode, half=half, f64=f64)
 
 
 @pytest.mark.parametrize("theta", [0.99, 0.95, 0.9, 0.7])
