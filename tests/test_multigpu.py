@@ -23,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, transport, mode, out_q, theta=0.9, nm=(8, 3), special=()):
+def _worker(rank, world, port, n, transport, mode, out_q, theta=0.9, nm=(8, 3), special=(), steps=4):
     import torch.distributed as dist
 
     import oracle as O
@@ -40,8 +40,7 @@ def _worker(rank, world, port, n, transport, mode, out_q, theta=0.9, nm=(8, 3), 
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        steps = 4
-        thetas = [theta, min(1.0, theta + 0.02), theta, min(1.0, theta + 0.05)]
+        thetas = [theta, min(1.0, theta + 0.02), theta, min(1.0, theta + 0.05)][:steps]
         rows = []                                # a different gradient on every step and rank
         for s in range(steps):
             rng = np.random.default_rng(77 + s)
@@ -58,7 +57,7 @@ def _worker(rank, world, port, n, transport, mode, out_q, theta=0.9, nm=(8, 3), 
         for s in range(steps):                  # the peer exchange alternates two gather buffers
             g = torch.from_numpy(rows[s][rank]).cuda()
             outs.append(avg.step(g, theta=thetas[s]).clone())
-        for s in (1, 2):                        # host-buffer step: same bits as the device step
+        for s in [s for s in (1, 2) if s < steps]:   # host-buffer step: same bits as the device step
             hout = avg.step_host(torch.from_numpy(rows[s][rank]).pin_memory(), theta=thetas[s])
             assert torch.equal(hout, outs[s].cpu()), "host step disagrees"
         avg.check()
@@ -106,6 +105,29 @@ def test_compressed_average_two_ranks(n, transport, mode):
         p.start()
     for p in procs:
         p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    res = [q.get(timeout=10) for _ in range(world)]
+    assert all(rel <= 1e-5 for _, rel, _ in res), res
+    assert len({d for _, _, d in res}) == 1, "ranks disagree bitwise"
+
+
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_c2_full_size_two_ranks(transport):
+    """BASELINE config 2 at its full size (25.6M floats per rank, 391 fused
+    chunks + the 40960-sample tail) over the exchange: 2 steps with different
+    gradients and theta; every rank's average within 1e-5 of the oracle
+    average of both ranks' messages, and bitwise equal across ranks."""
+    import torch.multiprocessing as mp
+    world, n = 2, 25_600_000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, transport, "count", q, 0.9, (8, 3), (), 2))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=900)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     res = [q.get(timeout=10) for _ in range(world)]
     assert all(rel <= 1e-5 for _, rel, _ in res), res
