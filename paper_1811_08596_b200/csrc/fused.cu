@@ -738,28 +738,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   // This CTA's half of the stream starts at global bit S = (r ? t0 : 0) * N;
   // staged in shared memory: local word k <-> global word (S >> 5) + k.
   const uint64_t S = r ? s1bits : 0ull;
-  if (N == 8 && !(dbg & 32u)) {
-    // byte codes: every code byte has one writer, so the codes go straight
-    // to the message (no staging, no zero fill, no copy-out); the half
-    // boundary is a byte boundary, and the bytes after the last code in its
-    // word are zeroed explicitly
-    uint8_t* cg8 = reinterpret_cast<uint8_t*>(codes_g);
-    const uint32_t cap_bytes = 4u * ci.code_cap;
-    uint32_t byte = (uint32_t)(S >> 3) + base;
+  if ((N == 8 || N == 16) && !(dbg & 32u)) {
+    // byte / halfword codes: every code unit has one writer, so the codes go
+    // straight to the message (no staging, no zero fill, no copy-out); the
+    // half boundary is a unit boundary, and the units after the last code in
+    // its word are zeroed explicitly
     const uint32_t* row = arr_own + pad(32u * tid);
-    auto emit8 = [&](uint64_t m64, const uint32_t* src) {
-      while (m64) {
-        const uint32_t pos = __ffsll((long long)m64) - 1;
-        m64 &= m64 - 1;
-        const uint32_t pc = src[pos >> 1];
-        if (byte < cap_bytes) cg8[byte] = (uint8_t)((pos & 1) ? (pc >> 16) : pc);
-        ++byte;
-      }
-    };
-    emit8(((uint64_t)w1 << 32) | w0, row);
-    if (w2) emit8(w2, arr_own + pad(32u * tid + 32u));
-    if (r == 1 && tid == 0)
-      for (uint32_t b = all; b < 4u * ((all + 3u) / 4u) && b < cap_bytes; ++b) cg8[b] = 0;
+    if (N == 8) {
+      uint8_t* cg = reinterpret_cast<uint8_t*>(codes_g);
+      const uint32_t cap_units = 4u * ci.code_cap;
+      uint32_t u = (uint32_t)(S >> 3) + base;
+      auto emit = [&](uint64_t m64, const uint32_t* src) {
+        while (m64) {
+          const uint32_t pos = __ffsll((long long)m64) - 1;
+          m64 &= m64 - 1;
+          const uint32_t pc = src[pos >> 1];
+          if (u < cap_units) cg[u] = (uint8_t)((pos & 1) ? (pc >> 16) : pc);
+          ++u;
+        }
+      };
+      emit(((uint64_t)w1 << 32) | w0, row);
+      if (w2) emit(w2, arr_own + pad(32u * tid + 32u));
+      if (r == 1 && tid == 0)
+        for (uint32_t b = all; b < 4u * ((all + 3u) / 4u) && b < cap_units; ++b) cg[b] = 0;
+    } else {
+      uint16_t* cg = reinterpret_cast<uint16_t*>(codes_g);
+      const uint32_t cap_units = 2u * ci.code_cap;
+      uint32_t u = (uint32_t)(S >> 4) + base;
+      auto emit = [&](uint64_t m64, const uint32_t* src) {
+        while (m64) {
+          const uint32_t pos = __ffsll((long long)m64) - 1;
+          m64 &= m64 - 1;
+          const uint32_t pc = src[pos >> 1];
+          if (u < cap_units) cg[u] = (uint16_t)((pos & 1) ? (pc >> 16) : pc);
+          ++u;
+        }
+      };
+      emit(((uint64_t)w1 << 32) | w0, row);
+      if (w2) emit(w2, arr_own + pad(32u * tid + 32u));
+      if (r == 1 && tid == 0 && (all & 1u) && all < cap_units) cg[all] = 0;
+    }
   } else {
   const uint32_t wstart = (uint32_t)(S >> 5), o = (uint32_t)(S & 31u);
   const uint32_t nwords = (uint32_t)((o + (uint64_t)total * N + 31) / 32);
