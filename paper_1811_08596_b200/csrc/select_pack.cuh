@@ -268,6 +268,8 @@ __device__ __noinline__ void select_pack_chunk(SelectSharedT<TH>& sh, const Chun
   const int N = q.n_bits;
   uint32_t rank_base = 0;     // codes emitted so far
   uint32_t origin = 0;        // global code word index of stage[0]
+  const bool direct = N == 8 || N == 16;         // whole-unit codes: no staging
+  const uint32_t cap_units = ci.code_cap * (32u / (uint32_t)(N == 8 ? 8 : 16));
   uint32_t tie_seen = 0;
   bool overflow = false;
   for (uint32_t s = tid; s < SelectSharedT<TH>::kStageWords; s += TH) sh.stage[s] = 0;
@@ -347,6 +349,25 @@ __device__ __noinline__ void select_pack_chunk(SelectSharedT<TH>& sh, const Chun
     }
     uint32_t ttot;
     const uint32_t r0 = rank_base + block_exclusive_scan<TH>(cnt, sh.scan, ttot);
+    if (direct) {
+      // byte / halfword codes: one writer per unit, straight into the message
+      uint32_t rr = r0;
+#pragma unroll
+      for (int u = 0; u < 2 * kPer; ++u) {
+        const uint32_t c = (u & 1) ? cim[u >> 1] : cre[u >> 1];
+        if (c) {
+          if (rr < cap_units) {
+            if (N == 8) reinterpret_cast<uint8_t*>(codes)[rr] = (uint8_t)c;
+            else reinterpret_cast<uint16_t*>(codes)[rr] = (uint16_t)c;
+          } else {
+            overflow = true;
+          }
+          ++rr;
+        }
+      }
+      rank_base += ttot;
+      continue;                                  // (the scan's closing barrier frees sh.scan)
+    }
     // stage the codes (LSB-first N-bit fields, bit 0 of stage[0] = word `origin`)
     const uint64_t obit = (uint64_t)origin * 32u;
     FGC_CHECK((uint64_t)(r0 + cnt) * N - obit <= 32ull * SelectSharedT<TH>::kStageWords);
@@ -376,7 +397,13 @@ __device__ __noinline__ void select_pack_chunk(SelectSharedT<TH>& sh, const Chun
     __syncthreads();
   }
   if (tid == 0) {
-    if ((uint64_t)rank_base * N & 31u) {
+    if (direct) {                                // the units after the last code in its word
+      const uint32_t per_word = 32u / (uint32_t)N;
+      for (uint32_t u = rank_base; u % per_word != 0 && u < cap_units; ++u) {
+        if (N == 8) reinterpret_cast<uint8_t*>(codes)[u] = 0;
+        else reinterpret_cast<uint16_t*>(codes)[u] = 0;
+      }
+    } else if ((uint64_t)rank_base * N & 31u) {
       if (origin < ci.code_cap) codes[origin] = sh.stage[0];
       else overflow = true;
     }
