@@ -175,7 +175,9 @@ struct __align__(16) CompressShared {
   float2 buf[kPadded + 64];          // FFT transposes / 4 sub-histograms / bin-ordered code half + staging
   float2 thi[256], tlo[kTloPadded];   // tlo and t1024 in tpad layout
   float2 t1024[kT1024Padded];
-  uint32_t hbm[1024 + 4];            // bitmap of this CTA's half (natural slot order), set during emit
+  uint32_t hbm[2048 + 4];            // bitmap words of the whole chunk, this CTA's (parity) bins only, set during
+                                     // emit with local atomics; the pack ORs in the peer's words
+
   uint32_t hist[2048];               // pass-1 histogram of this CTA (read by the peer)
   uint32_t hist2[2048];              // pass-2 histogram of this CTA (read by the peer)
   uint32_t scan[40];
@@ -347,7 +349,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   reinterpret_cast<uint4*>(sh.hist2)[tid] = make_uint4(0, 0, 0, 0);
   sh.hbm[tid] = 0u;
   sh.hbm[tid + 512] = 0u;
-  if (tid < 4) sh.hbm[1024 + tid] = 0u;
+  sh.hbm[tid + 1024] = 0u;
+  sh.hbm[tid + 1536] = 0u;
+  if (tid < 4) sh.hbm[2048 + tid] = 0u;
   if (tid == 0) { sh.ccount = 0; sh.below = 0; sh.anynz = 0; sh.rcount[0] = 0; sh.rcount[1] = 0; }
   uint32_t* codes_g = DEBUG ? nullptr : reinterpret_cast<uint32_t*>(a.message + ci.seg_off + ci.code_off);
   __syncthreads();
@@ -613,13 +617,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
         const uint32_t lb = bin - d * kHalfBins;
         FGC_CHECK(lb <= kHalfBins && pad(lb) < kStageOff);
         const uint32_t bits = ((cre ? 1u : 0u) | (cim ? 2u : 0u)) << (2u * (lb & 15u));
-        if (d == r) {
-          arr_own[pad(lb)] = pc;
-          atomicOr(&sh.hbm[lb >> 4], bits);
-        } else {
-          arr_peer[pad(lb)] = pc;
-          atomicOr(&shp.hbm[lb >> 4], bits);
-        }
+        atomicOr(&sh.hbm[(lb >> 4) + d * 1024u], bits);
+        if (d == r) arr_own[pad(lb)] = pc;
+        else arr_peer[pad(lb)] = pc;
       }
     }
   };
@@ -681,13 +681,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
           const uint32_t lb = bin - d * kHalfBins;
           FGC_CHECK(lb <= kHalfBins && pad(lb) < kStageOff);
           const uint32_t bits = ((cre ? 1u : 0u) | (cim ? 2u : 0u)) << (2u * (lb & 15u));
-          if (d == r) {
-            arr_own[pad(lb)] = pc;
-            atomicOr(&sh.hbm[lb >> 4], bits);
-          } else {
-            arr_peer[pad(lb)] = pc;
-            atomicOr(&shp.hbm[lb >> 4], bits);
-          }
+          atomicOr(&sh.hbm[(lb >> 4) + d * 1024u], bits);      // local: the pack merges both CTAs' words
+          if (d == r) arr_own[pad(lb)] = pc;
+          else arr_peer[pad(lb)] = pc;
         }
       }
       __syncwarp();                               // strip reused by the next round
@@ -712,14 +708,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   // byte-aligned half boundary (N = 8, 16, or t0*N % 8 == 0): no cross-CTA fold needed
   const uint64_t s1bits = (uint64_t)t0 * N;
   const bool fold = (s1bits & 7u) != 0;
-  // Without a fold this was the last remote access: arrive now, wait before
-  // exiting (a CTA's shared memory must outlive its peer's accesses).
-  if (!fold) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-
   // ---- 6. pack: thread t of CTA d owns bins d*16384 + [32t, 32t+32) (+ bin N)
   const uint32_t nb = (r == 1 && tid == kThreads - 1) ? 33u : 32u;
-  // the bitmap was built during emit; only the set slots of the code arrays are valid
-  const uint32_t w0 = sh.hbm[2 * tid], w1 = sh.hbm[2 * tid + 1], w2 = (nb == 33) ? sh.hbm[1024] : 0u;
+  // the bitmap words of my bins: both CTAs' (disjoint, parity-interleaved)
+  // bits; only the set slots of the code arrays are valid
+  const uint32_t gw = r * 1024u + 2u * tid;
+  const uint32_t w0 = sh.hbm[gw] | shp.hbm[gw], w1 = sh.hbm[gw + 1] | shp.hbm[gw + 1];
+  const uint32_t w2 = (nb == 33) ? (sh.hbm[2048] | shp.hbm[2048]) : 0u;
+  // Without a fold these were the last remote accesses: arrive now, wait
+  // before exiting (a CTA's shared memory must outlive its peer's accesses).
+  if (!fold) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   const uint32_t cnt = __popc(w0) + __popc(w1) + __popc(w2);
   uint32_t* seg = reinterpret_cast<uint32_t*>(a.message + ci.seg_off);
   uint32_t* bm = seg + kSegHeader / 4;
