@@ -1297,7 +1297,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_fused
   const float scale = 1.0f / (float)kN;
   float* out = a.out + ci.in_off;
   float dbg_sum = 0.f;
-  for (uint32_t c = 0; c < 2; ++c) {
+#pragma unroll
+  for (uint32_t c = 0; c < 2; ++c) {                        // (unrolled: the two columns' loads overlap)
     const uint32_t k = tid + 512u * c;
     float2 o[16];
     fft_pass3<true>(k, sh.x, o, sh.thi, sh.tlo);
